@@ -1,0 +1,190 @@
+/*
+ * polar_b200.h -- C ABI of libpolar_b200.so, the B200 (sm_100a) kernels of
+ * Polar Sparsity's batched-decode hot path.
+ *
+ * Conventions (every entry point):
+ *   - stream-ordered: work is enqueued on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream); nothing synchronises the host;
+ *   - the library never allocates: outputs and workspaces are caller-owned
+ *     device buffers whose sizes come from the *_workspace_bytes queries,
+ *     which keeps every call CUDA-graph capturable;
+ *   - data: bf16 activations/weights/KV (uint16 bit patterns), f32 logits
+ *     and accumulators, int32 indices and lengths;
+ *   - return value: PS_OK or a PS_ERR_* status (ps_status_string() names
+ *     it).  Host-visible argument errors are detected before any launch.
+ *
+ * The reference (`sparsedecode`, /root/reference/pkg) has no FFI: its
+ * operator API is the set of Python functions re-exported by
+ * sparsedecode/__init__.py:18-75 and bound by name in engine.py:25-35.  Each
+ * entry point below names the reference function it replaces; the Python
+ * package paper_2505_14884_b200 mirrors those names on top of this ABI.
+ */
+#ifndef POLAR_B200_H
+#define POLAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map 1:1 onto the reference's exception types) ---- */
+#define PS_OK               0
+#define PS_ERR_VALUE        1  /* ValueError  (shapes, k range, scale <= 0) */
+#define PS_ERR_INDEX        2  /* IndexError  (ids out of range)            */
+#define PS_ERR_EMPTY_CACHE  3  /* EmptyCacheError (exceptions.py:4-5)       */
+#define PS_ERR_CAPACITY     4  /* CapacityError   (exceptions.py:8-9)       */
+#define PS_ERR_UNSUPPORTED  5  /* ValueError: shape not built for sm_100a   */
+#define PS_ERR_WORKSPACE    6  /* ValueError: workspace too small           */
+#define PS_ERR_CUDA         7  /* RuntimeError: CUDA launch/config failure  */
+
+#define PS_DTYPE_F32  0
+#define PS_DTYPE_BF16 1
+
+#define PS_ACT_NONE 0
+#define PS_ACT_RELU 1
+
+int ps_version(void);
+const char* ps_status_string(int status);
+/* number of SMs of the current device (grid sizing helper) */
+int ps_num_sms(void);
+
+/* ======================================================================
+ * Select-Head Attention (SHA) decode
+ * Replaces sparsedecode.kernels.gqa_selective_attention_decode
+ * (kernels.py:513-548 -> _attention_over_units 386-444) and, for G == 1,
+ * selective_head_flash_attention_decode (kernels.py:464-510).
+ *
+ *   q       bf16 (B, H, d_h), row b at q + b*q_ld elements (q_ld >= H*d_h)
+ *   k_cache bf16 (B, H_kv, cap, d_h) contiguous; v_cache likewise
+ *   lengths int32 (B,): rows [0, lengths[b]) are valid; others never read
+ *   sel     int32 (B, top_k): selected KV-group ids per sequence (distinct,
+ *           in [0, H_kv); query heads g*G .. g*G+G-1, G = H/H_kv, attend)
+ *   out     (B, H, d_h) f32 or bf16, row b at out + b*out_ld elements;
+ *           heads of non-selected groups are written as exact 0.0
+ *   group_base  tensor parallelism: this rank's cache/q/out hold global groups
+ *           [group_base, group_base + H_kv); selected ids outside that range
+ *           are skipped (0 without TP)
+ *   num_splits  KV splits per (b, group) unit (FlashDecoding); 0 = auto
+ *   ws      >= ps_sha_workspace_bytes(...) bytes; must be zero-filled
+ *           before its first use (the kernel leaves it zeroed again)
+ * ==================================================================== */
+size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int top_k, int num_splits);
+int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_len);
+int ps_sha_decode(const void* q, int64_t q_ld,
+                  const void* k_cache, const void* v_cache,
+                  const int32_t* lengths, const int32_t* sel, int group_base,
+                  int B, int H, int H_kv, int cap, int d_h, int top_k,
+                  float scale, int num_splits, int max_len_hint,
+                  void* out, int64_t out_ld, int out_dtype,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* ======================================================================
+ * KV cache append for one decode step.
+ * Replaces sparsedecode.tensors.KVCache.append_step (tensors.py:150-170):
+ * writes k_new/v_new (B, H_kv, d_h) bf16 (row b at +b*src_ld elements) at
+ * position lengths[b] and increments lengths[b].  A sequence already at
+ * capacity is left untouched and err_flag (int32, may be NULL) is set to 1.
+ * ==================================================================== */
+int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths,
+                 const void* k_new, const void* v_new, int64_t src_ld,
+                 int B, int H_kv, int cap, int d_h, int32_t* err_flag, void* stream);
+
+/* ======================================================================
+ * Selection (bit-exact with the reference ordering: value descending,
+ * ties -> lower index, -0.0 == +0.0, NaN below -inf).
+ * ps_topk_rows replaces tensors.topk_indices_rows (tensors.py:65-73) and
+ * BatchHeadIndex.from_logits (kernels.py:107-112); ids are written
+ * ascending.  `bitmap` (may be NULL) additionally receives an atomic OR of
+ * every selected id (bit i of word i/32) -- the union's first half.
+ * ps_threshold_rows is the router's predict() (routers.py:188-190, logit >
+ * thr) ORed into the bitmap.
+ * ps_union_rows ORs an id matrix into the bitmap; ps_bitmap_compact
+ * replaces union_neuron_indices (kernels.py:376-383): ascending ids of the
+ * set bits in [lo, hi) minus lo (lo % 32 == 0; lo=0, hi=width for the whole
+ * union, a neuron shard's range under tensor parallelism) and the
+ * device-resident count, padding idx_out up to a multiple of `pad` with the
+ * last id, and clearing the bitmap for the next call.  Bitmaps must be
+ * zero-filled before first use; words = ceil(width/32).
+ * ==================================================================== */
+int ps_topk_rows(const float* logits, int rows, int cols, int64_t ld, int k,
+                 int32_t* idx_out, uint32_t* bitmap, void* stream);
+int ps_threshold_rows(const float* logits, int rows, int cols, int64_t ld, float thr,
+                      uint32_t* bitmap, void* stream);
+int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width,
+                  uint32_t* bitmap, void* stream);
+int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, int pad,
+                      int32_t* idx_out, int32_t* count_out, void* stream);
+
+/* ======================================================================
+ * Head router fused with its top-k.
+ * Replaces HeadRouter.decision_function (routers.py:324-325, 178-186)
+ * followed by BatchHeadIndex.from_logits (kernels.py:107-112), as called
+ * in engine.py:352-357.
+ *   x      bf16 (B, d), row b at +b*x_ld;  w_t bf16 (H_kv, d) (= W^T);
+ *   bias   f32 (H_kv) or NULL;  logits_out f32 (B, H_kv) or NULL;
+ *   sel_out int32 (B, k) ascending.
+ * ==================================================================== */
+int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const float* bias,
+                        int B, int d, int H_kv, int k,
+                        float* logits_out, int32_t* sel_out, void* stream);
+
+/* ======================================================================
+ * Gathered GEMM on tcgen05 tensor cores (TMEM accumulators).
+ *
+ * ps_gather_gemm  ("rows" form; replaces selective_gemm, kernels.py:268-291,
+ * the up-projection half of sparse_mlp_forward 353-373, and -- with
+ * idx == NULL -- the dense router layers routers.py:286-288):
+ *   out[n, j] = act( sum_k w_rows[idx[j], k] * x[n, k] + bias[idx[j]] )
+ *               (+ residual[n, j] if residual != NULL, added after act)
+ *   for j < count (count = *count_dev if count_dev else M), n < N;
+ *   columns j in [count, M_pad) of out are written as 0.
+ *   w_rows bf16 (rows, K) row-major (neuron-major);  x bf16 (N, K) row b at
+ *   +b*x_ld;  out (N, M_pad) f32/bf16 row n at +n*out_ld.
+ *
+ * ps_gather_gemm_t ("contraction" form; replaces selective_gemm_t,
+ * kernels.py:294-310, and the down-projection of sparse_mlp_forward):
+ *   out[n, m] = sum_{j < count} h[n, j] * w_rows[idx[j], m] + bias[m]
+ *               (+ residual[n, m] if residual != NULL)
+ *   w_rows bf16 (rows, M) row-major;  h bf16 (N, K_pad) row n at +n*h_ld
+ *   with K_pad >= count rounded up to 64 and zero beyond count.
+ *
+ * idx is int32 (NULL = identity), padded to a multiple of 128 entries
+ * (ps_bitmap_compact(pad=128) produces this).  Requirements: K % 8 == 0 for
+ * the rows form, M % 8 == 0 for the contraction form, 16-byte aligned rows.
+ * ws >= ps_gather_gemm_workspace_bytes(...) and zero-filled before first use.
+ * ==================================================================== */
+size_t ps_gather_gemm_workspace_bytes(int N, int M, int K, int splits);
+int ps_gather_gemm_auto_splits(int N, int M, int K);
+int ps_gather_gemm(const void* w_rows, const int32_t* idx, const int32_t* count_dev,
+                   const void* x, int64_t x_ld, const float* bias,
+                   const float* residual, int64_t residual_ld,
+                   int N, int M, int K, int act, int splits,
+                   void* out, int64_t out_ld, int out_dtype,
+                   void* ws, size_t ws_bytes, void* stream);
+int ps_gather_gemm_t(const void* w_rows, const int32_t* idx, const int32_t* count_dev,
+                     const void* h, int64_t h_ld, const float* bias, const float* residual,
+                     int64_t residual_ld, int N, int M, int K_max, int splits,
+                     void* out, int64_t out_ld, int out_dtype,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* ======================================================================
+ * Decode-step glue.
+ * ps_layernorm: model.layernorm (model.py:168-175): x f32 (B, d) row b at
+ *   +b*x_ld -> y bf16 (B, d), eps 1e-5, f32 statistics.
+ * ps_embed: x[b] = embed[tokens[b]] + pos_embed[lengths[b]] (engine.py:342),
+ *   f32 out, bf16 tables.
+ * ==================================================================== */
+int ps_layernorm(const float* x, int64_t x_ld, const float* gamma, const float* beta,
+                 int B, int d, void* y, int64_t y_ld, void* stream);
+/* ps_swiglu: the gated activation of swiglu_mlp_forward (kernels.py:335-350):
+ *   h[b, j] = silu(gu[b, j]) * gu[b, D + j]   (bf16 in/out, f32 math)     */
+int ps_swiglu(const void* gu, int64_t gu_ld, int B, int D, void* h, int64_t h_ld, void* stream);
+int ps_embed(const int32_t* tokens, const int32_t* lengths, const void* embed,
+             const void* pos_embed, int B, int d, float* x, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLAR_B200_H */

@@ -1,0 +1,161 @@
+// Decode-step glue around the hot path + library metadata.
+//   * ps_kv_append  -- KVCache.append_step (tensors.py:150-170)
+//   * ps_layernorm  -- model.layernorm (model.py:168-175)
+//   * ps_embed      -- token + position embedding (engine.py:342)
+#include "common.cuh"
+
+namespace ps {
+namespace {
+
+// one CTA per sequence: copy H_kv*d_h new keys/values to row lengths[b],
+// then bump lengths[b].  A full sequence is left untouched (err_flag = 1).
+__global__ void kv_append_kernel(uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int32_t* __restrict__ lengths,
+                                 const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn, int64_t src_ld,
+                                 int H_kv, int cap, int d_h, int32_t* err_flag) {
+  const int b = blockIdx.x;
+  const int pos = lengths[b];
+  if (pos >= cap) {
+    if (threadIdx.x == 0 && err_flag) *err_flag = 1;
+    return;
+  }
+  const int vec_per_head = d_h / 8;
+  const int total = H_kv * vec_per_head;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int h = e / vec_per_head, c = e - h * vec_per_head;
+    const size_t dst = (((size_t)b * H_kv + h) * cap + pos) * d_h + c * 8;
+    const size_t src = (size_t)b * src_ld + (size_t)h * d_h + c * 8;
+    *reinterpret_cast<uint4*>(kc + dst) = *reinterpret_cast<const uint4*>(kn + src);
+    *reinterpret_cast<uint4*>(vc + dst) = *reinterpret_cast<const uint4*>(vn + src);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) lengths[b] = pos + 1;
+}
+
+constexpr int kLnThreads = 256;
+
+__global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const float* __restrict__ x, int64_t x_ld,
+                                                               const float* __restrict__ g,
+                                                               const float* __restrict__ bta, int d,
+                                                               uint16_t* __restrict__ y, int64_t y_ld) {
+  __shared__ float red[2][kLnThreads / 32];
+  const float* xr = x + (size_t)blockIdx.x * x_ld;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < d; i += kLnThreads) s += xr[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = s;
+  __syncthreads();
+  float mean = 0.f;
+#pragma unroll
+  for (int w = 0; w < kLnThreads / 32; ++w) mean += red[0][w];
+  mean /= d;
+  float v = 0.f;
+  for (int i = threadIdx.x; i < d; i += kLnThreads) {
+    const float t = xr[i] - mean;
+    v += t * t;
+  }
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[1][threadIdx.x >> 5] = v;
+  __syncthreads();
+  float var = 0.f;
+#pragma unroll
+  for (int w = 0; w < kLnThreads / 32; ++w) var += red[1][w];
+  var /= d;
+  const float rstd = rsqrtf(var + 1e-5f);
+  uint16_t* yr = y + (size_t)blockIdx.x * y_ld;
+  for (int i = threadIdx.x; i < d; i += kLnThreads) yr[i] = f2bf((xr[i] - mean) * rstd * g[i] + bta[i]);
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ len,
+                             const uint16_t* __restrict__ emb, const uint16_t* __restrict__ pos, int d,
+                             float* __restrict__ x) {
+  const int b = blockIdx.x;
+  const uint16_t* er = emb + (size_t)tok[b] * d;
+  const uint16_t* pr = pos + (size_t)len[b] * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    x[(size_t)b * d + i] = __uint_as_float((uint32_t)er[i] << 16) + __uint_as_float((uint32_t)pr[i] << 16);
+}
+
+// h = silu(gate) * up, gate/up from one (B, 2D) bf16 row [gate | up]
+__global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int64_t gu_ld, int B, int D,
+                              uint16_t* __restrict__ h, int64_t h_ld) {
+  const int64_t total = (int64_t)B * D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / D), j = (int)(e - (int64_t)b * D);
+    const float g = __uint_as_float((uint32_t)gu[(size_t)b * gu_ld + j] << 16);
+    const float u = __uint_as_float((uint32_t)gu[(size_t)b * gu_ld + D + j] << 16);
+    h[(size_t)b * h_ld + j] = f2bf(g / (1.f + __expf(-g)) * u);
+  }
+}
+
+}  // namespace
+
+int g_num_sms = 0;
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" int ps_version(void) { return 1; }
+
+extern "C" const char* ps_status_string(int status) {
+  switch (status) {
+    case PS_OK: return "ok";
+    case PS_ERR_VALUE: return "invalid argument";
+    case PS_ERR_INDEX: return "index out of range";
+    case PS_ERR_EMPTY_CACHE: return "empty KV cache";
+    case PS_ERR_CAPACITY: return "KV cache capacity exhausted";
+    case PS_ERR_UNSUPPORTED: return "shape not supported by the sm_100a kernels";
+    case PS_ERR_WORKSPACE: return "workspace too small";
+    case PS_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+extern "C" int ps_num_sms(void) {
+  if (g_num_sms == 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      g_num_sms = n;
+    else
+      return 148;
+  }
+  return g_num_sms;
+}
+
+extern "C" int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths, const void* k_new, const void* v_new,
+                            int64_t src_ld, int B, int H_kv, int cap, int d_h, int32_t* err_flag, void* stream) {
+  if (B < 1 || H_kv < 1 || cap < 1 || d_h < 8 || d_h % 8 || src_ld < (int64_t)H_kv * d_h || src_ld % 8)
+    return PS_ERR_VALUE;
+  if (!k_cache || !v_cache || !lengths || !k_new || !v_new) return PS_ERR_VALUE;
+  kv_append_kernel<<<B, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths, static_cast<const uint16_t*>(k_new),
+      static_cast<const uint16_t*>(v_new), src_ld, H_kv, cap, d_h, err_flag);
+  return launch_status();
+}
+
+extern "C" int ps_layernorm(const float* x, int64_t x_ld, const float* gamma, const float* beta, int B, int d,
+                            void* y, int64_t y_ld, void* stream) {
+  if (B < 1 || d < 1 || !x || !gamma || !beta || !y || x_ld < d || y_ld < d) return PS_ERR_VALUE;
+  layernorm_kernel<<<B, kLnThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, x_ld, gamma, beta, d,
+                                                                            static_cast<uint16_t*>(y), y_ld);
+  return launch_status();
+}
+
+extern "C" int ps_embed(const int32_t* tokens, const int32_t* lengths, const void* embed, const void* pos_embed,
+                        int B, int d, float* x, void* stream) {
+  if (B < 1 || d < 1 || !tokens || !lengths || !embed || !pos_embed || !x) return PS_ERR_VALUE;
+  embed_kernel<<<B, 256, 0, static_cast<cudaStream_t>(stream)>>>(tokens, lengths,
+                                                                 static_cast<const uint16_t*>(embed),
+                                                                 static_cast<const uint16_t*>(pos_embed), d, x);
+  return launch_status();
+}
+
+extern "C" int ps_swiglu(const void* gu, int64_t gu_ld, int B, int D, void* h, int64_t h_ld, void* stream) {
+  if (B < 1 || D < 1 || !gu || !h || gu_ld < 2 * (int64_t)D || h_ld < D) return PS_ERR_VALUE;
+  const int64_t total = (int64_t)B * D;
+  int grid = (int)((total + 255) / 256);
+  if (grid > 148 * 16) grid = 148 * 16;
+  swiglu_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint16_t*>(gu), gu_ld, B, D,
+                                                                     static_cast<uint16_t*>(h), h_ld);
+  return launch_status();
+}

@@ -1,0 +1,200 @@
+"""Router forward passes on B200 -- drop-in for ``sparsedecode.routers``
+forward API (routers.py:154-341).
+
+Training (BCE + AdamW, supervision collection) stays in the reference: it is
+offline CPU work.  A router trained there is moved here
+with ``from_reference(router)``; a router built here with the same seed
+draws the reference's exact initial weights (routers.py:280-284, 320-322).
+Weights are stored bf16 on the device; logits are f32.
+
+* :class:`HeadRouter` -- ``logits = x W + b`` fused with the per-row top-k
+  (one launch, ``select``), routers.py:306-331.
+* :class:`MlpRouter` -- ``relu(x W_in + b_in) W_out + b_out`` as two tcgen05
+  GEMM launches, routers.py:256-303; ``select_topk`` / ``select_threshold``
+  write the batch union straight into a device bitmap.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib, _ws
+from .kernels import BatchHeadIndex, NeuronIndexTensor, ROW_PAD, _round_up, gather_gemm_into
+from .validation import as_device_tensor, check_count, default_device
+
+
+def _as_batch(x, d, device):
+    t = as_device_tensor(x, "x", device=device)
+    single = t.ndim == 1
+    if single:
+        t = t[None, :]
+    if t.ndim != 2:
+        raise ValueError(f"expected vector or batch of vectors, got {tuple(t.shape)}")
+    if t.shape[1] != d:
+        raise ValueError(f"expected {d} features, got {t.shape[1]}")
+    return t.to(torch.bfloat16).contiguous(), single
+
+
+class HeadRouter:
+    """Single linear layer scoring heads / KV groups (routers.py:306-331)."""
+
+    def __init__(self, d_model: int, n_heads: int, seed: int = 0, device=None, _weights=None):
+        check_count(d_model, "d_model")
+        check_count(n_heads, "n_heads")
+        self.d_model, self.n_heads, self.seed = d_model, n_heads, seed
+        if _weights is None:
+            rng = np.random.default_rng(seed)
+            w = rng.normal(0.0, 1.0 / math.sqrt(d_model), (d_model, n_heads))
+            b = np.zeros(n_heads)
+        else:
+            w, b = _weights
+        dev = device or default_device()
+        self.w_t = torch.as_tensor(np.ascontiguousarray(np.asarray(w, np.float64).T), dtype=torch.float32).to(
+            dev, torch.bfloat16).contiguous()
+        self.b = torch.as_tensor(np.asarray(b, np.float64), dtype=torch.float32).to(dev)
+        self._scratch = None
+
+    @classmethod
+    def from_reference(cls, router, device=None) -> "HeadRouter":
+        return cls(router.w_.shape[0], router.w_.shape[1], getattr(router, "seed", 0), device,
+                   _weights=(router.w_, router.b_))
+
+    @classmethod
+    def from_weights(cls, w, b, device=None) -> "HeadRouter":
+        w = np.asarray(w)
+        return cls(w.shape[0], w.shape[1], 0, device, _weights=(w, b))
+
+    def select_into(self, x2d: torch.Tensor, k: int, sel_out: torch.Tensor, logits_out=None) -> None:
+        B, d = x2d.shape
+        _lib.call("ps_head_router_topk", _lib.ptr(x2d), x2d.stride(0), _lib.ptr(self.w_t), _lib.ptr(self.b),
+                  B, d, self.n_heads, int(k), _lib.ptr(logits_out), _lib.ptr(sel_out), _lib.stream_ptr())
+
+    def decision_function(self, x) -> torch.Tensor:
+        """routers.py:178-186: per-head logits (f32), vector or batch."""
+        xb, single = _as_batch(x, self.d_model, self.w_t.device)
+        B = xb.shape[0]
+        logits = torch.empty((B, self.n_heads), dtype=torch.float32, device=xb.device)
+        sel = torch.empty((B, 1), dtype=torch.int32, device=xb.device)
+        self.select_into(xb, 1, sel, logits)
+        return logits[0] if single else logits
+
+    def predict(self, x) -> torch.Tensor:
+        return self.decision_function(x) > 0.0
+
+    def select(self, x, k: int) -> BatchHeadIndex:
+        """Fused router + top-k -> BatchHeadIndex (engine.py:352-357)."""
+        xb, _ = _as_batch(x, self.d_model, self.w_t.device)
+        if not 1 <= k <= self.n_heads:
+            raise ValueError(f"k must be in [1, {self.n_heads}], got {k}")
+        sel = torch.empty((xb.shape[0], k), dtype=torch.int32, device=xb.device)
+        self.select_into(xb, k, sel)
+        return BatchHeadIndex(sel, validate=False, n_max=self.n_heads)
+
+
+class MlpRouter:
+    """Two-layer ReLU neuron-activity predictor (routers.py:256-303)."""
+
+    def __init__(self, d_model: int, ffn_dim: int, hidden_dim: int | None = None, seed: int = 0,
+                 device=None, _weights=None):
+        check_count(d_model, "d_model")
+        check_count(ffn_dim, "ffn_dim")
+        h = hidden_dim if hidden_dim is not None else min(1024, 4 * d_model)
+        check_count(h, "hidden_dim")
+        self.d_model, self.ffn_dim, self.hidden_dim_, self.seed = d_model, ffn_dim, h, seed
+        if _weights is None:
+            rng = np.random.default_rng(seed)
+            w_in = rng.normal(0.0, math.sqrt(2.0 / d_model), (d_model, h))
+            w_out = rng.normal(0.0, math.sqrt(2.0 / h), (h, ffn_dim))
+            b_in, b_out = np.zeros(h), np.zeros(ffn_dim)
+        else:
+            w_in, b_in, w_out, b_out = _weights
+        dev = device or default_device()
+        f32 = lambda a: torch.as_tensor(np.asarray(a, np.float64), dtype=torch.float32)  # noqa: E731
+        self.w_in_t = f32(np.asarray(w_in).T).to(dev, torch.bfloat16).contiguous()    # (h, d)
+        self.b_in = f32(b_in).to(dev)
+        self.w_out_t = f32(np.asarray(w_out).T).to(dev, torch.bfloat16).contiguous()  # (D, h)
+        self.b_out = f32(b_out).to(dev)
+
+    @classmethod
+    def from_reference(cls, router, device=None) -> "MlpRouter":
+        return cls(router.w_in_.shape[0], router.w_out_.shape[1], router.w_in_.shape[1],
+                   getattr(router, "seed", 0), device,
+                   _weights=(router.w_in_, router.b_in_, router.w_out_, router.b_out_))
+
+    @classmethod
+    def from_weights(cls, w_in, b_in, w_out, b_out, device=None) -> "MlpRouter":
+        w_in = np.asarray(w_in)
+        return cls(w_in.shape[0], np.asarray(w_out).shape[1], w_in.shape[1], 0, device,
+                   _weights=(w_in, b_in, w_out, b_out))
+
+    def logits_into(self, x2d: torch.Tensor, hid: torch.Tensor, logits: torch.Tensor) -> None:
+        """Two tcgen05 launches: hid = relu(x W_in + b_in) (bf16), logits (f32)."""
+        B, d = x2d.shape
+        h = self.hidden_dim_
+        gather_gemm_into(self.w_in_t, None, None, x2d, x2d.stride(0), self.b_in, B, h, d, _lib.PS_ACT_RELU,
+                         hid, hid.stride(0), tag="gg_router")
+        gather_gemm_into(self.w_out_t, None, None, hid, hid.stride(0), self.b_out, B, self.ffn_dim, h,
+                         _lib.PS_ACT_NONE, logits, logits.stride(0), tag="gg_router")
+
+    def decision_function(self, x) -> torch.Tensor:
+        xb, single = _as_batch(x, self.d_model, self.w_in_t.device)
+        B = xb.shape[0]
+        if self.hidden_dim_ % 8:
+            raise ValueError("router hidden width must be a multiple of 8 on the GPU path")
+        hid = torch.empty((B, self.hidden_dim_), dtype=torch.bfloat16, device=xb.device)
+        logits = torch.empty((B, self.ffn_dim), dtype=torch.float32, device=xb.device)
+        self.logits_into(xb, hid, logits)
+        return logits[0] if single else logits
+
+    def predict(self, x) -> torch.Tensor:
+        """routers.py:188-190: sigmoid(logit) > 0.5, i.e. logit > 0."""
+        return self.decision_function(x) > 0.0
+
+    def select_topk(self, x, k: int, layer: int = 0) -> NeuronIndexTensor:
+        """Per-row top-k of the logits, unioned over the batch (engine.py:371-376)."""
+        logits = self.decision_function(x)
+        if logits.ndim == 1:
+            logits = logits[None, :]
+        return union_from_logits(logits, k=k, layer=layer)
+
+    def select_threshold(self, x, threshold: float = 0.0, layer: int = 0) -> NeuronIndexTensor:
+        logits = self.decision_function(x)
+        if logits.ndim == 1:
+            logits = logits[None, :]
+        return union_from_logits(logits, threshold=threshold, layer=layer)
+
+
+def union_from_logits(logits: torch.Tensor, k: int | None = None, threshold: float | None = None,
+                      layer: int = 0) -> NeuronIndexTensor:
+    """Top-k (or threshold) selection per row, ORed into a bitmap and
+    compacted into the ascending batch union -- all on the device."""
+    rows, width = logits.shape
+    logits = logits.contiguous().float()
+    dev = logits.device
+    bitmap = _ws.get("union_bitmap", ((width + 31) // 32) * 4, dev)
+    if k is not None:
+        if not 1 <= k <= width:
+            raise ValueError(f"k must be in [1, {width}], got {k}")
+        _lib.call("ps_topk_rows", _lib.ptr(logits), rows, width, width, int(k), None, _lib.ptr(bitmap),
+                  _lib.stream_ptr())
+    else:
+        _lib.call("ps_threshold_rows", _lib.ptr(logits), rows, width, width, float(threshold or 0.0),
+                  _lib.ptr(bitmap), _lib.stream_ptr())
+    buf = torch.empty(_round_up(width, ROW_PAD), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("ps_bitmap_compact", _lib.ptr(bitmap), width, 0, width, ROW_PAD, _lib.ptr(buf), _lib.ptr(cnt),
+              _lib.stream_ptr())
+    return NeuronIndexTensor(layer, buf, cnt)
+
+
+def mlp_router_forward(router: MlpRouter, x) -> torch.Tensor:
+    """routers.py:334-336."""
+    return router.decision_function(x)
+
+
+def head_router_forward(router: HeadRouter, x) -> torch.Tensor:
+    """routers.py:339-341."""
+    return router.decision_function(x)

@@ -1,0 +1,187 @@
+"""Device substrate: the KV cache and the bit-exact top-k.
+
+Mirrors ``sparsedecode.tensors`` (tensors.py:24-213) on B200: the cache
+keeps the reference's (B, H_kv, capacity, d_h) layout -- every selected
+(sequence, KV group) history is one contiguous slab, which is what lets the
+SHA kernel stage it with bulk async copies -- but stores bf16 K/V and int32
+lengths in HBM.  A host mirror of ``lengths`` lets capacity / empty-cache
+errors be raised before launch without a device sync.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .exceptions import CapacityError
+from .validation import as_device_tensor, check_count
+
+MATMUL_TILE = 256  # tensors.py:24-26 (kept for API parity)
+
+
+def _rows_topk(scores: torch.Tensor, k: int) -> torch.Tensor:
+    scores = scores.contiguous()
+    if scores.dtype != torch.float32:
+        scores = scores.float()
+    rows, cols = scores.shape
+    out = torch.empty((rows, k), dtype=torch.int32, device=scores.device)
+    _lib.call("ps_topk_rows", _lib.ptr(scores), rows, cols, cols, k, _lib.ptr(out), None,
+              _lib.stream_ptr())
+    return out
+
+
+def topk_indices_rows(scores, k: int) -> torch.Tensor:
+    """tensors.py:65-73: row-wise top-k, ascending ids, ties to the lower index.
+
+    Bit-exact with the reference given identical f32 scores (-0.0 == +0.0,
+    NaN ranks below -inf).  Returns int32 (rows, k) on the scores' device.
+    """
+    s = as_device_tensor(scores, "scores")
+    if s.ndim != 2:
+        raise ValueError(f"scores must be 2-dimensional, got shape {tuple(s.shape)}")
+    if not 1 <= k <= s.shape[1]:
+        raise ValueError(f"k must be in [1, {s.shape[1]}], got {k}")
+    return _rows_topk(s, int(k))
+
+
+def topk_indices(scores, k: int) -> torch.Tensor:
+    """tensors.py:54-62: 1-D top-k with the same tie rule."""
+    s = as_device_tensor(scores, "scores")
+    if s.ndim != 1:
+        raise ValueError(f"scores must be 1-dimensional, got shape {tuple(s.shape)}")
+    if not 1 <= k <= s.shape[0]:
+        raise ValueError(f"k must be in [1, {s.shape[0]}], got {k}")
+    return _rows_topk(s[None, :], int(k))[0]
+
+
+class KVCache:
+    """Per-layer K/V history in HBM (tensors.py:116-213 semantics).
+
+    ``keys``/``values``: bf16 (batch, kv_heads, capacity, head_dim);
+    ``lengths``: int32 device vector; ``host_lengths``: int64 numpy mirror.
+    """
+
+    def __init__(self, batch: int, kv_heads: int, capacity: int, head_dim: int,
+                 device="cuda", dtype=torch.bfloat16):
+        check_count(batch, "batch")
+        check_count(kv_heads, "kv_heads")
+        check_count(capacity, "capacity")
+        check_count(head_dim, "head_dim")
+        if dtype != torch.bfloat16:
+            raise ValueError("the B200 cache stores bf16 K/V")
+        shape = (batch, kv_heads, capacity, head_dim)
+        self.keys = torch.zeros(shape, dtype=dtype, device=device)
+        self.values = torch.zeros(shape, dtype=dtype, device=device)
+        self.lengths = torch.zeros(batch, dtype=torch.int32, device=device)
+        self.host_lengths = np.zeros(batch, dtype=np.int64)
+        self._err = torch.zeros(1, dtype=torch.int32, device=device)
+
+    @property
+    def batch(self) -> int:
+        return self.keys.shape[0]
+
+    @property
+    def kv_heads(self) -> int:
+        return self.keys.shape[1]
+
+    @property
+    def capacity(self) -> int:
+        return self.keys.shape[2]
+
+    @property
+    def head_dim(self) -> int:
+        return self.keys.shape[3]
+
+    @property
+    def device(self):
+        return self.keys.device
+
+    def _sync_lengths(self) -> None:
+        self.lengths.copy_(torch.from_numpy(self.host_lengths.astype(np.int32)))
+
+    def append_step(self, k_new, v_new, src_ld=None) -> None:
+        """tensors.py:150-170 -- one token for every sequence (device kernel).
+
+        ``k_new``/``v_new``: (batch, kv_heads, head_dim) bf16 CUDA tensors, or
+        row-strided views (``src_ld`` elements between sequences).
+        """
+        if (self.host_lengths >= self.capacity).any():
+            raise CapacityError(f"KV cache capacity {self.capacity} exhausted")
+        k_new = as_device_tensor(k_new, "k_new", dtype=torch.bfloat16)
+        v_new = as_device_tensor(v_new, "v_new", dtype=torch.bfloat16)
+        if src_ld is None:
+            expect = (self.batch, self.kv_heads, self.head_dim)
+            if tuple(k_new.shape) != expect or tuple(v_new.shape) != expect:
+                raise ValueError(f"append_step expects shape {expect}")
+            k_new, v_new = k_new.contiguous(), v_new.contiguous()
+            src_ld = self.kv_heads * self.head_dim
+        _lib.call("ps_kv_append", _lib.ptr(self.keys), _lib.ptr(self.values), _lib.ptr(self.lengths),
+                  _lib.ptr(k_new), _lib.ptr(v_new), int(src_ld), self.batch, self.kv_heads,
+                  self.capacity, self.head_dim, _lib.ptr(self._err), _lib.stream_ptr())
+        self.host_lengths += 1
+
+    def append_tokens(self, b: int, k_tokens, v_tokens) -> None:
+        """tensors.py:172-192 -- a run of tokens for one sequence (prefill)."""
+        k_tokens = as_device_tensor(k_tokens, "k_tokens", dtype=torch.bfloat16, device=self.device)
+        v_tokens = as_device_tensor(v_tokens, "v_tokens", dtype=torch.bfloat16, device=self.device)
+        t = k_tokens.shape[0]
+        if tuple(k_tokens.shape[1:]) != (self.kv_heads, self.head_dim):
+            raise ValueError("k_tokens shape mismatch with cache")
+        start = int(self.host_lengths[b])
+        if start + t > self.capacity:
+            raise CapacityError(f"sequence {b}: {start}+{t} tokens exceed capacity {self.capacity}")
+        self.keys[b, :, start:start + t] = k_tokens.transpose(0, 1)
+        self.values[b, :, start:start + t] = v_tokens.transpose(0, 1)
+        self.host_lengths[b] = start + t
+        self._sync_lengths()
+
+    def set_lengths(self, lengths) -> None:
+        lengths = np.asarray(lengths, dtype=np.int64).reshape(self.batch)
+        if (lengths < 0).any() or (lengths > self.capacity).any():
+            raise ValueError("lengths out of range")
+        self.host_lengths[:] = lengths
+        self._sync_lengths()
+
+    def fill_random(self, rng, length: int) -> None:
+        """tensors.py:201-213 -- synthetic N(0,1) history.
+
+        ``rng`` may be a numpy Generator (reproduces the reference's exact
+        draws, host-side, for parity tests) or a torch.Generator / int seed
+        (drawn on the device, for benchmark-sized caches).
+        """
+        if not 1 <= length <= self.capacity:
+            raise ValueError(f"length must be in [1, {self.capacity}]")
+        shape = (self.batch, self.kv_heads, length, self.head_dim)
+        if isinstance(rng, np.random.Generator):
+            k = rng.standard_normal(shape, dtype=np.float32)
+            v = rng.standard_normal(shape, dtype=np.float32)
+            self.keys[:, :, :length] = torch.from_numpy(k).to(self.device, torch.bfloat16)
+            self.values[:, :, :length] = torch.from_numpy(v).to(self.device, torch.bfloat16)
+        else:
+            gen = rng if isinstance(rng, torch.Generator) else None
+            if gen is None:
+                gen = torch.Generator(device=self.device)
+                gen.manual_seed(int(rng) if rng is not None else 0)
+            self.keys[:, :, :length].normal_(generator=gen)
+            self.values[:, :, :length].normal_(generator=gen)
+        self.host_lengths[:] = length
+        self._sync_lengths()
+
+    def keys_for(self, b: int, h: int) -> torch.Tensor:
+        return self.keys[b, h, : int(self.host_lengths[b])]
+
+    def values_for(self, b: int, h: int) -> torch.Tensor:
+        return self.values[b, h, : int(self.host_lengths[b])]
+
+
+def l2_norm_per_head(attn_out) -> torch.Tensor:
+    """tensors.py:76-80 (study helper; plain torch on device)."""
+    a = as_device_tensor(attn_out, "attn_out")
+    return torch.linalg.vector_norm(a[:, :, 0, :].double(), dim=-1).float()
+
+
+def rsqrt_head_dim(d_h: int) -> float:
+    return 1.0 / math.sqrt(d_h)
