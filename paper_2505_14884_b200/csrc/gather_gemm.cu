@@ -35,7 +35,7 @@ constexpr int BK = 64;    // K elements per stage (one 128-byte swizzle row)
 constexpr int kEpiThreads = 128;
 constexpr int kThreads = 160;  // warps 0-3 producer+epilogue, warp 4 MMA
 constexpr int kMaxNB = 256;
-constexpr int kTicketBytes = 4096;
+constexpr int kTicketBytes = 65536;
 
 enum { MODE_UP = 0, MODE_DOWN = 1 };
 

@@ -30,7 +30,11 @@ constexpr int kThreads = 128;
 constexpr int kWarps = 4;
 constexpr int kStages = 4;
 constexpr int kTileBytes = 8192;  // bytes of one K (or V) tile
-constexpr int kCounterBytes = 256;
+// Fixed-size ticket region at the head of the workspace: its layout must not
+// depend on the launch shape, or a previous launch's partials would alias
+// another shape's tickets (they are only zero where the last CTA reset them).
+constexpr int kMaxUnits = 65536;
+constexpr size_t kCounterBytes = (size_t)kMaxUnits * 4;
 
 template <int D_H>
 struct ShaShape {
@@ -361,8 +365,7 @@ extern "C" size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int to
   if (B < 1 || H_kv < 1 || top_k < 1 || H % H_kv) return 0;
   if (num_splits < 1) num_splits = 1;
   const size_t units = (size_t)B * top_k;
-  size_t counters = (units * 4 + kCounterBytes - 1) / kCounterBytes * kCounterBytes;
-  return counters + units * num_splits * (size_t)partial_floats(H / H_kv, d_h) * 4;
+  return kCounterBytes + units * num_splits * (size_t)partial_floats(H / H_kv, d_h) * 4;
 }
 
 extern "C" int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_len) {
@@ -387,6 +390,7 @@ extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, c
                              int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
   if (B < 1 || H < 1 || H_kv < 1 || cap < 1 || top_k < 1 || group_base < 0) return PS_ERR_VALUE;
   if (H % H_kv) return PS_ERR_VALUE;
+  if ((int64_t)B * top_k > kMaxUnits) return PS_ERR_UNSUPPORTED;
   if (!(scale > 0.f)) return PS_ERR_VALUE;
   if (q_ld < (int64_t)H * d_h || out_ld < (int64_t)H * d_h) return PS_ERR_VALUE;
   if (!q || !k_cache || !v_cache || !lengths || !sel || !out || !ws) return PS_ERR_VALUE;
@@ -409,8 +413,7 @@ extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, c
   prm.out_ld = out_ld;
   const size_t units = (size_t)B * top_k;
   prm.counters = static_cast<int*>(ws);
-  prm.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
-                                          (units * 4 + kCounterBytes - 1) / kCounterBytes * kCounterBytes);
+  prm.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes);
   const int grid = (int)(units * num_splits) + B;
   const bool bf16 = out_dtype == PS_DTYPE_BF16;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

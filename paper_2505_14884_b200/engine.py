@@ -1,0 +1,333 @@
+"""Batched decode step on B200 -- the caller of the hot path.
+
+Restates ``sparsedecode.engine.decode_step`` (engine.py:314-392) with the
+same policy semantics (``SparsityPolicy``: modes dense / dejavu_mlp / polar,
+head budget ceil(rho*H_kv - 1e-9), layer 0 dense by default, sparse MLP only
+for ReLU models with a k table) and the same per-layer order:
+
+    LN1 -> QKV -> KV append -> [head router -> top-k] -> SHA -> O-proj(+res)
+        -> LN2 -> [MLP router -> per-row top-k -> union] -> selective MLP(+res)
+
+Every launch is a libpolar_b200 kernel on static buffers, so the whole step
+is captured once into a CUDA graph and replayed (the paper measured with
+CUDA graphs).  The host only keeps the length mirror used for
+capacity checks.  Tensor parallelism (heads + neurons sharded, routers
+replicated, all-reduce after the O- and down-projections) lives in
+``parallel.py`` and reuses :meth:`DecodeEngine.step_launches`.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, _ws
+from .exceptions import CapacityError, ConfigurationError
+from .kernels import ROW_PAD, _round_up, gather_gemm_into, mlp_into, sha_decode_into, swiglu_into
+from .model import DeviceModel, TransformerConfig
+from .tensors import KVCache
+from .validation import check_choice, check_count
+
+_MODES = ("dense", "dejavu_mlp", "polar")
+
+
+@dataclass(frozen=True)
+class SparsityPolicy:
+    """engine.py:42-77 (router ranking only; the oracle-norm ranking is a
+    study tool that computes every head and gives no speedup)."""
+
+    mode: str = "dense"
+    mlp_k_table: object = None
+    head_density: float = 1.0
+    layer0_dense_attention: bool = True
+
+    def __post_init__(self):
+        check_choice(self.mode, _MODES, "mode")
+        if not 0.0 < float(self.head_density) <= 1.0:
+            raise ValueError(f"head_density must be in (0, 1], got {self.head_density}")
+
+    def head_budget(self, n_route: int) -> int:
+        return max(1, math.ceil(self.head_density * n_route - 1e-9))
+
+    def wants_sparse_mlp(self, config: TransformerConfig) -> bool:
+        if self.mode == "dense" or config.activation != "relu":
+            return False
+        return self.mlp_k_table is not None
+
+    def wants_sparse_heads(self, layer: int) -> bool:
+        if self.mode != "polar":
+            return False
+        if layer == 0 and self.layer0_dense_attention:
+            return False
+        return self.head_density < 1.0
+
+    def k_for(self, layer: int) -> int:
+        t = self.mlp_k_table
+        if hasattr(t, "k_for"):
+            return int(t.k_for(layer))  # calibration.LayerKTable (calibration.py:64-68)
+        try:
+            return int(t[layer])
+        except (KeyError, IndexError, TypeError) as exc:
+            raise ConfigurationError(f"no calibrated k for layer {layer}") from exc
+
+
+class DecodeEngine:
+    """Decode session + step for one GPU (or one tensor-parallel rank).
+
+    ``kv_ring``: number of distinct per-layer K/V storage buffers.  Default =
+    layers.  A smaller ring aliases K/V STORAGE round-robin for shapes whose
+    full cache exceeds HBM; every layer keeps its own lengths and reads its
+    full (selected) history, so bytes moved and kernel work are unchanged --
+    only capacity is saved (SURVEY.md §7 hard parts; reported in bench.py).
+    """
+
+    def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
+                 head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None):
+        cfg = model.config
+        check_count(batch, "batch")
+        check_count(capacity, "capacity")
+        self.model, self.cfg, self.B, self.policy = model, cfg, batch, policy
+        self.head_routers, self.mlp_routers = head_routers, mlp_routers
+        self.tp = tp
+        dev = model.device
+        self.device = dev
+        d, dk, H, H_kv, d_h = cfg.model_dim, cfg.kv_dim, cfg.heads, cfg.kv_heads, cfg.head_dim
+        # TP: local head / group / neuron counts (parallel.py fills tp)
+        self.H_loc = H if tp is None else tp.heads_local
+        self.Hkv_loc = H_kv if tp is None else tp.kv_heads_local
+        self.group_base = 0 if tp is None else tp.group_base
+        self.d_loc = self.H_loc * d_h
+        self.dk_loc = self.Hkv_loc * d_h
+        self.sparse_mlp = policy.wants_sparse_mlp(cfg)
+        if policy.mode == "dejavu_mlp" and not self.sparse_mlp:
+            raise ConfigurationError("dejavu_mlp mode requires a ReLU model and a calibrated k table")
+        # per-layer selection budgets (validated up front: ConfigurationError like engine.py:294-301)
+        self.k_heads = []
+        self.k_mlp = []
+        for ell in range(cfg.layers):
+            if policy.wants_sparse_heads(ell):
+                if head_routers is None or len(head_routers) <= ell or head_routers[ell] is None:
+                    raise ConfigurationError(f"no head router available for layer {ell}")
+                self.k_heads.append(policy.head_budget(H_kv))
+            else:
+                self.k_heads.append(0)
+            if self.sparse_mlp:
+                if mlp_routers is None or len(mlp_routers) <= ell or mlp_routers[ell] is None:
+                    raise ConfigurationError(f"no neuron router available for layer {ell}")
+                self.k_mlp.append(min(policy.k_for(ell), cfg.ffn_dim))
+            else:
+                self.k_mlp.append(0)
+        # KV caches (optionally aliased storage)
+        ring = cfg.layers if kv_ring is None else max(1, min(kv_ring, cfg.layers))
+        self.kv_ring = ring
+        base = [KVCache(batch, self.Hkv_loc, capacity, d_h, device=dev) for _ in range(ring)]
+        self.caches = []
+        for ell in range(cfg.layers):
+            c = base[ell % ring]
+            if ell >= ring:
+                alias = KVCache.__new__(KVCache)
+                alias.keys, alias.values = c.keys, c.values
+                alias.lengths = torch.zeros(batch, dtype=torch.int32, device=dev)
+                alias.host_lengths = np.zeros(batch, dtype=np.int64)
+                alias._err = torch.zeros(1, dtype=torch.int32, device=dev)
+                c = alias
+            self.caches.append(c)
+        # static activation buffers (graph-capturable)
+        f32, bf = torch.float32, torch.bfloat16
+        D = cfg.ffn_dim
+        self.D_loc = D if tp is None else tp.ffn_local
+        self.x = torch.zeros(batch, d, dtype=f32, device=dev)
+        self.h = torch.zeros(batch, d, dtype=bf, device=dev)
+        qkv_w = self.d_loc + 2 * self.dk_loc
+        self.qkv = torch.zeros(batch, qkv_w, dtype=bf, device=dev)
+        self.attn = torch.zeros(batch, self.d_loc, dtype=bf, device=dev)
+        self.hidden = torch.zeros(batch, _round_up(self.D_loc, ROW_PAD), dtype=bf, device=dev)
+        self.gu = torch.zeros(batch, 2 * self.D_loc, dtype=bf, device=dev) if cfg.activation == "swiglu" else None
+        self.tokens = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.logits = torch.zeros(batch, cfg.vocab, dtype=f32, device=dev)
+        self.next_tokens = torch.zeros(batch, dtype=torch.int64, device=dev)
+        self.sel_full = torch.arange(H_kv, dtype=torch.int32, device=dev).repeat(batch, 1).contiguous()
+        kmax = max(self.k_heads + [1])
+        self.sel = torch.zeros(batch, kmax, dtype=torch.int32, device=dev)
+        if self.sparse_mlp:
+            h_r = mlp_routers[0].hidden_dim_
+            self.r_hid = torch.zeros(batch, h_r, dtype=bf, device=dev)
+            self.r_logits = torch.zeros(batch, D, dtype=f32, device=dev)
+            self.bitmap = torch.zeros((D + 31) // 32, dtype=torch.int32, device=dev)
+            self.union_idx = torch.zeros(_round_up(D, ROW_PAD), dtype=torch.int32, device=dev)
+            self.union_count = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.union_counts = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
+        self.scale = 1.0 / math.sqrt(d_h)
+        self.graph = None
+        self.launches_per_step = None
+        self.record = None  # eager-only debug capture of selections (parity tests)
+
+    # ------------------------------------------------------------------ state
+    @property
+    def host_lengths(self) -> np.ndarray:
+        return self.caches[0].host_lengths
+
+    def fill_random(self, length: int, seed: int = 0) -> None:
+        """bench.py:70-100 synthetic_session: N(0,1) history of ``length``."""
+        gen = torch.Generator(device=self.device)
+        gen.manual_seed(seed)
+        for ell, c in enumerate(self.caches):
+            if ell < self.kv_ring:
+                c.fill_random(gen, length)
+            else:
+                c.host_lengths[:] = length
+                c.lengths.fill_(length)
+
+    def _check_capacity(self) -> None:
+        if (self.host_lengths >= self.cfg.max_seq).any():
+            raise CapacityError("position table exhausted (max_seq reached)")
+        for c in self.caches:
+            if (c.host_lengths >= c.capacity).any():
+                raise CapacityError(f"KV cache capacity {c.capacity} exhausted")
+            if (c.host_lengths < 0).any():
+                raise ValueError("negative cache length")
+
+    # ------------------------------------------------------------------ launches
+    def _allreduce(self, t: torch.Tensor) -> None:
+        if self.tp is not None:
+            self.tp.all_reduce(t)
+
+    def step_launches(self) -> int:
+        """Enqueue one decode step on the current stream; returns the number
+        of libpolar_b200 kernel launches enqueued."""
+        cfg, m, B = self.cfg, self.model, self.B
+        d = cfg.model_dim
+        n = 0
+        st = _lib.stream_ptr()
+        L = _lib.load()
+        _lib.check(L.ps_embed(_lib.ptr(self.tokens), _lib.ptr(self.caches[0].lengths), _lib.ptr(m.embed),
+                              _lib.ptr(m.pos_embed), B, d, _lib.ptr(self.x), st), "ps_embed")
+        n += 1
+        qkv_w = self.qkv.shape[1]
+        for ell, lw in enumerate(m.layers):
+            c = self.caches[ell]
+            _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(lw.ln1_g), _lib.ptr(lw.ln1_b), B, d,
+                                      _lib.ptr(self.h), d, st), "ps_layernorm")
+            gather_gemm_into(lw.w_qkv_t, None, None, self.h, d, lw.b_qkv, B, qkv_w, d, _lib.PS_ACT_NONE,
+                             self.qkv, qkv_w, tag="gg_qkv")
+            kq = self.qkv[:, self.d_loc:]
+            vq = self.qkv[:, self.d_loc + self.dk_loc:]
+            _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths), _lib.ptr(kq),
+                                      _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity, cfg.head_dim,
+                                      _lib.ptr(c._err), st), "ps_kv_append")
+            n += 3
+            k_h = self.k_heads[ell]
+            if k_h:
+                sel = self.sel[:, :k_h]
+                if k_h != self.sel.shape[1]:
+                    sel = self.sel_bufs(k_h)
+                hl = None
+                if self.record is not None:
+                    hl = torch.empty(B, cfg.kv_heads, dtype=torch.float32, device=self.device)
+                self.head_routers[ell].select_into(self.h, k_h, sel, hl)
+                n += 1
+                if self.record is not None:
+                    self.record.setdefault("head_logits", []).append(hl)
+                    self.record.setdefault("heads", []).append(sel.clone())
+            else:
+                sel = self.sel_full
+            sha_decode_into(self.qkv, qkv_w, c, sel, self.H_loc, self.scale, self.attn, self.d_loc,
+                            group_base=self.group_base, max_len_hint=int(c.host_lengths.max()) + 1)
+            n += 1
+            if self.tp is None:
+                gather_gemm_into(lw.w_o_t, None, None, self.attn, self.d_loc, lw.b_o, B, d, self.d_loc,
+                                 _lib.PS_ACT_NONE, self.x, d, residual=self.x, res_ld=d, tag="gg_o")
+            else:
+                self.tp.o_proj(self, lw)
+            n += 1
+            _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(lw.ln2_g), _lib.ptr(lw.ln2_b), B, d,
+                                      _lib.ptr(self.h), d, st), "ps_layernorm")
+            n += 1
+            if self.sparse_mlp:
+                self.mlp_routers[ell].logits_into(self.h, self.r_hid, self.r_logits)
+                _lib.check(L.ps_topk_rows(_lib.ptr(self.r_logits), B, cfg.ffn_dim, cfg.ffn_dim, self.k_mlp[ell],
+                                          None, _lib.ptr(self.bitmap), st), "ps_topk_rows")
+                lo, hi = (0, cfg.ffn_dim) if self.tp is None else self.tp.ffn_range
+                _lib.check(L.ps_bitmap_compact(_lib.ptr(self.bitmap), cfg.ffn_dim, lo, hi, ROW_PAD,
+                                               _lib.ptr(self.union_idx), _lib.ptr(self.union_count), st),
+                           "ps_bitmap_compact")
+                n += 4
+                idx, cnt = self.union_idx, self.union_count
+                if self.record is not None:
+                    self.record.setdefault("mlp_logits", []).append(self.r_logits.clone())
+                    self.record.setdefault("union", []).append(self.union_idx[: int(cnt.item())].clone())
+            else:
+                idx = cnt = None
+            resid = self.x if self.tp is None else None
+            if self.tp is None:
+                if cfg.activation == "swiglu":
+                    swiglu_into(lw.mlp, self.h, self.gu, self.hidden, self.x, residual=self.x)
+                    n += 3
+                else:
+                    mlp_into(lw.mlp, self.h, idx, cnt, self.hidden, self.x, residual=resid)
+                    n += 2
+            else:
+                n += self.tp.mlp(self, lw, idx, cnt)
+        _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(m.lnf_g), _lib.ptr(m.lnf_b), B, d,
+                                  _lib.ptr(self.h), d, st), "ps_layernorm")
+        gather_gemm_into(m.unembed_t, None, None, self.h, d, None, B, cfg.vocab, d, _lib.PS_ACT_NONE,
+                         self.logits, cfg.vocab, tag="gg_lm")
+        n += 2
+        torch.argmax(self.logits, dim=1, out=self.next_tokens)
+        return n
+
+    def sel_bufs(self, k: int) -> torch.Tensor:
+        key = f"_sel_{k}"
+        buf = getattr(self, key, None)
+        if buf is None:
+            buf = torch.zeros(self.B, k, dtype=torch.int32, device=self.device)
+            setattr(self, key, buf)
+        return buf
+
+    def _advance(self) -> None:
+        for c in self.caches:
+            c.host_lengths += 1
+
+    # ------------------------------------------------------------------ public
+    def step(self, tokens=None) -> torch.Tensor:
+        """engine.py:314-392: advance every sequence by one token; returns the
+        (B, vocab) f32 logits (device).  Uses the captured graph if any."""
+        self._check_capacity()
+        if tokens is not None:
+            tk = torch.as_tensor(np.asarray(tokens) if not isinstance(tokens, torch.Tensor) else tokens)
+            if tuple(tk.shape) != (self.B,):
+                raise ValueError(f"tokens must have shape ({self.B},), got {tuple(tk.shape)}")
+            if int(tk.min()) < 0 or int(tk.max()) >= self.cfg.vocab:
+                raise IndexError(f"tokens contains indices >= {self.cfg.vocab}")
+            self.tokens.copy_(tk.to(torch.int32), non_blocking=True)
+        else:
+            self.tokens.copy_(self.next_tokens.to(torch.int32))
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.launches_per_step = self.step_launches()
+        self._advance()
+        return self.logits
+
+    def capture(self, warmup: int = 1) -> None:
+        """Capture one step into a CUDA graph (workspaces sized by a warm-up
+        step first; the warm-up's KV writes are undone via the lengths)."""
+        saved = [c.host_lengths.copy() for c in self.caches]
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.launches_per_step = self.step_launches()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        for c, hl in zip(self.caches, saved):
+            c.host_lengths[:] = hl
+            c.lengths.copy_(torch.from_numpy(hl.astype(np.int32)))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.step_launches()
+        torch.cuda.synchronize()
+        self.graph = g
