@@ -1,0 +1,426 @@
+"""Decode throughput benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config opt-6.7b] [--batch 64] [--ctx 1920] [--rho 0.5] [--union 0.5]
+
+Metric (BASELINE.json): decode tokens/s (polar sparse step) vs the dense
+step, at the OPT-6.7B shape (configs[1]) by default: random-init weights
+N(0, 0.02), synthetic N(0,1) KV history of ``ctx`` tokens, batch 64, head
+density rho=0.5 (16 of 32 heads from the head router's top-k; layer 0
+dense), union neuron density |S|/D set by a hot-neuron router bias
+(SURVEY.md §7).  A "step" = one full 32-layer decode step (embed -> 32 x
+[LN, QKV, KV append, head router+top-k, SHA, O-proj, LN, MLP router,
+top-k, union, selective MLP] -> LN -> LM head -> argmax), replayed from one
+CUDA graph.  Inputs exceed L2 (64 GB of KV), so no explicit L2 flush.
+
+* value        -- polar tok/s, device-timed (CUDA events), max over ranks;
+* dense        -- the same kernels at full density (rho=1, every neuron);
+* e2e          -- the public engine API with HOST token buffers: per step a
+                  pinned H2D copy of the tokens, graph replay, D2H of the next
+                  tokens and a host sync, all inside the timed region;
+* roofline     -- the SHA kernel (dominant) timed alone on the same caches:
+                  algorithmic bytes / CUDA-event duration vs
+                  MEASURED_PEAKS.json hbm_gbs;
+* cpu_baseline -- the oracle (numpy port of the reference, f32/f64 on the
+                  host cores) on one decode layer of the same workload, x L.
+
+``--impl reference`` runs only the reference arm: the oracle port of the
+reference CPU path (there is no GPU reference implementation), rank 0 only.
+N > 1 (torchrun): every rank decodes its own batch (data-parallel replicas,
+weak scaling, no data-path collective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="opt-6.7b")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--ctx", type=int, default=1920)
+    ap.add_argument("--rho", type=float, default=0.5)
+    ap.add_argument("--union", type=float, default=0.5, help="target |S|/D of the MLP union")
+    ap.add_argument("--kv-ring", type=int, default=0, help="alias KV storage over this many buffers (0 = auto)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU (oracle) leg
+def cpu_layer_sample(cfg, batch, ctx, rho, union, reps=2, warm=1, seed=0):
+    """One decode layer of the workload on the host with the oracle (numpy
+    restatement of the reference, f32 storage / f64 accumulation); returns
+    seconds per layer (median of ``reps``)."""
+    from oracle import polar_oracle as po
+
+    rng = np.random.default_rng(seed)
+    d, D, H, H_kv, d_h = cfg.model_dim, cfg.ffn_dim, cfg.heads, cfg.kv_heads, cfg.head_dim
+    dk = H_kv * d_h
+    g = lambda *s: rng.standard_normal(s, dtype=np.float32) * np.float32(0.02)  # noqa: E731
+    lw = dict(ln1_g=np.ones(d, np.float32), ln1_b=np.zeros(d, np.float32), w_q=g(d, d), b_q=np.zeros(d, np.float32),
+              w_k=g(d, dk), b_k=np.zeros(dk, np.float32), w_v=g(d, dk), b_v=np.zeros(dk, np.float32),
+              w_o=g(d, d), b_o=np.zeros(d, np.float32), ln2_g=np.ones(d, np.float32),
+              ln2_b=np.zeros(d, np.float32), mlp_w1=g(d, D), mlp_b1=g(D), mlp_w2=g(d, D),
+              mlp_b2=np.zeros(d, np.float32))
+    h_r = min(1024, 4 * d)
+    hr = {"w": rng.standard_normal((d, H_kv)) / math.sqrt(d), "b": np.zeros(H_kv)}
+    mr = {"w_in": rng.standard_normal((d, h_r), dtype=np.float32) * np.float32(math.sqrt(2 / d)),
+          "b_in": np.zeros(h_r), "w_out": rng.standard_normal((h_r, D), dtype=np.float32) * np.float32(math.sqrt(2 / h_r)),
+          "b_out": np.zeros(D)}
+    k_mlp = max(1, int(union * D))
+    hot = rng.choice(D, k_mlp, replace=False)
+    mr["b_out"][hot] += 20.0
+    cache = po.KVCache(batch, H_kv, ctx + warm + reps + 1, d_h)
+    cache.fill_random(rng, ctx)
+    x = rng.standard_normal((batch, d), dtype=np.float32)
+    k_h = po.head_budget(rho, H_kv)
+    scale = 1.0 / math.sqrt(d_h)
+
+    def layer():
+        h1 = po.layernorm(x, lw["ln1_g"], lw["ln1_b"])
+        q4 = (po.matmul(h1, lw["w_q"]) + lw["b_q"]).reshape(batch, H, d_h)[:, :, None, :]
+        kk = (po.matmul(h1, lw["w_k"]) + lw["b_k"]).reshape(batch, H_kv, d_h)
+        vv = (po.matmul(h1, lw["w_v"]) + lw["b_v"]).reshape(batch, H_kv, d_h)
+        cache.append_step(kk, vv)
+        sel = po.topk_indices_rows(po.head_router_forward(hr["w"], hr["b"], h1), k_h)
+        attn = po.gqa_selective_attention_decode(q4, cache, sel, 64, scale)
+        x2 = x + (po.matmul(attn[:, :, 0, :].reshape(batch, d), lw["w_o"]) + lw["b_o"])
+        h2 = po.layernorm(x2, lw["ln2_g"], lw["ln2_b"])
+        logits = po.mlp_router_forward(mr["w_in"], mr["b_in"], mr["w_out"], mr["b_out"], h2)
+        union_idx = po.union_neuron_indices(list(po.topk_indices_rows(logits, k_mlp)))
+        y = po.sparse_mlp_forward(h2[:, None, :], lw["mlp_w1"], lw["mlp_b1"], lw["mlp_w2"], lw["mlp_b2"],
+                                  union_idx)
+        return x2 + y[:, 0, :]
+
+    for _ in range(warm):
+        layer()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        layer()
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts))
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2505_14884_b200.model import SHAPES
+
+    cfg = SHAPES[args.config]
+    batch = args.cpu_batch or args.batch
+    per_layer = []
+    # each "step" = one decode layer timed on the host, x L layers
+    t_setup = time.perf_counter()
+    s = cpu_layer_sample(cfg, batch, args.ctx, args.rho, args.union, reps=args.steps, warm=min(args.warmup, 3))
+    per_layer.append(s)
+    step_s = s * cfg.layers
+    value = batch / step_s
+    sample = (f"oracle port of the reference (numpy f32/f64), one decode layer of {args.config} "
+              f"B={batch} ctx={args.ctx} rho={args.rho} |S|/D={args.union}, median of {args.steps} "
+              f"(after {min(args.warmup, 3)} warm-up), x {cfg.layers} layers")
+    line = {"impl": "reference", "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "data": "synthetic", "config": workload_config(args, cfg),
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cpu_threads(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_setup}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, cfg):
+    return {"workload": f"{args.config} polar decode step", "model_shape": args.config, "global_batch": args.batch,
+            "seq_len": args.ctx, "head_density": args.rho, "union_density": args.union,
+            "layers": cfg.layers, "d_model": cfg.model_dim, "ffn": cfg.ffn_dim, "heads": cfg.heads,
+            "kv_heads": cfg.kv_heads, "parallelism": f"dp{args.gpus}",
+            "l2": "inputs larger than L2 (KV cache >> 126 MB); no flush"}
+
+
+# ---------------------------------------------------------------- our arm
+def sha_algorithmic_bytes(lengths, k_h, G, d_h, B, H):
+    """selected K+V rows + Q + O (zeros included) + ids + lengths."""
+    kv = float(np.sum(lengths)) * k_h * d_h * 2 * 2
+    return kv + B * k_h * G * d_h * 2 + B * H * d_h * 2 + B * k_h * 4 + B * 4
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2505_14884_b200 as pb
+    from paper_2505_14884_b200 import _lib, kernels as pk
+    from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy
+    from paper_2505_14884_b200.model import SHAPES, DeviceModel
+
+    cfg = SHAPES[args.config]
+    B, ctx = args.batch, args.ctx
+    L, H, H_kv, d_h, D = cfg.layers, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.ffn_dim
+    cap = ctx + args.warmup * 2 + args.steps * 3 + 8
+    kv_layer = B * H_kv * cap * d_h * 2 * 2
+    free = torch.cuda.mem_get_info(dev)[0]
+    model = DeviceModel.random(cfg, seed=1234 + rank, device=dev)
+    budget = free - model.weight_bytes() - 12 * 2 ** 30
+    ring = args.kv_ring or (L if kv_layer * L <= budget else max(2, int(budget // kv_layer)))
+    ring = min(ring, L)
+
+    k_h = math.ceil(args.rho * H_kv - 1e-9)
+    k_mlp = max(1, int(round(args.union * D)))
+    gen = np.random.default_rng(7 + rank)
+    sparse_relu = cfg.activation == "relu"
+    hr = [pb.HeadRouter(cfg.model_dim, H_kv, seed=100 + ell, device=dev) for ell in range(L)]
+    mr = None
+    if sparse_relu:
+        mr = [pb.MlpRouter.random_device(cfg.model_dim, D, seed=200 + ell, device=dev,
+                                         hot=gen.choice(D, k_mlp, replace=False)) for ell in range(L)]
+    polar = SparsityPolicy(mode="polar", head_density=args.rho,
+                           mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
+    eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring)
+    eng.fill_random(ctx, seed=99 + rank)
+    dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches)
+    tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()
+    out_host = torch.empty(B, dtype=torch.int64).pin_memory()
+    eng.tokens.copy_(tokens_host)
+    dense.tokens.copy_(tokens_host)
+    eng.capture()
+    dense.capture()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        barrier()
+        ms = s.elapsed_time(e)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    def replay(engine):
+        def f():
+            engine.graph.replay()
+            engine._advance()
+        return f
+
+    # warm-up
+    for _ in range(args.warmup):
+        replay(dense)()
+        replay(eng)()
+    torch.cuda.synchronize()
+    ms_dense = timed(replay(dense), args.steps)
+    with ClockSampler(local) as clk:
+        ms_polar = timed(replay(eng), args.steps)
+    clocks = clk.summary()
+
+    # union density actually used (device count of the last layer, read after timing)
+    union_density = None
+    if sparse_relu:
+        union_density = int(eng.union_count.item()) / D
+
+    # e2e: host tokens in, host next-tokens out, through the engine API
+    def e2e_step():
+        eng.tokens.copy_(tokens_host, non_blocking=True)
+        eng.graph.replay()
+        eng._advance()
+        out_host.copy_(eng.next_tokens, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    ms_e2e = timed(e2e_step, args.steps)
+    wall_e2e = (time.perf_counter() - t0) * 1e3
+
+    # roofline: the SHA kernel alone on the same caches, one launch per layer
+    qkv = eng.qkv
+    sel = torch.stack([torch.randperm(H_kv, device=dev)[:k_h].sort().values for _ in range(B)]).to(torch.int32)
+    out = torch.empty(B, cfg.model_dim, dtype=torch.bfloat16, device=dev)
+    lens = [c.host_lengths.copy() for c in eng.caches]
+    for c in eng.caches[:2]:
+        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H, eng.scale, out, cfg.model_dim,
+                           max_len_hint=int(c.host_lengths.max()))
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s_ev.record(st)
+    for c in eng.caches:
+        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H, eng.scale, out, cfg.model_dim,
+                           max_len_hint=int(c.host_lengths.max()))
+    e_ev.record(st)
+    torch.cuda.synchronize()
+    sha_ms = s_ev.elapsed_time(e_ev) / L
+    sha_bytes = float(np.mean([sha_algorithmic_bytes(l, k_h, H // H_kv, d_h, B, H) for l in lens]))
+    hbm_peak, _, peak_kind = load_peaks()
+    achieved = sha_bytes / (sha_ms * 1e-3) / 1e9
+
+    # selective MLP kernels alone (UP + DOWN gathered GEMMs), one per layer
+    mlp_ms = None
+    mlp_bytes = None
+    if sparse_relu:
+        x2 = torch.randn(B, cfg.model_dim, device=dev).to(torch.bfloat16)
+        y = torch.empty(B, cfg.model_dim, dtype=torch.float32, device=dev)
+        hot_idx = torch.from_numpy(np.sort(gen.choice(D, k_mlp, replace=False))).to(dev, torch.int32)
+        nit = pb.NeuronIndexTensor(0, hot_idx, validate=False)
+        hidden = eng.hidden
+        pk.mlp_into(model.layers[0].mlp, x2, nit.buffer, nit.count, hidden, y)
+        torch.cuda.synchronize()
+        s_ev.record(st)
+        for lw in model.layers:
+            pk.mlp_into(lw.mlp, x2, nit.buffer, nit.count, hidden, y)
+        e_ev.record(st)
+        torch.cuda.synchronize()
+        mlp_ms = s_ev.elapsed_time(e_ev) / L
+        mlp_bytes = 2 * k_mlp * cfg.model_dim * 2 + k_mlp * 4 + cfg.model_dim * 4 + 2 * B * cfg.model_dim * 2 + k_mlp * 4
+
+    line = None
+    if rank == 0:
+        toks = world * B * args.steps
+        value = toks / (ms_polar * 1e-3)
+        dense_value = toks / (ms_dense * 1e-3)
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cb = args.cpu_batch or B
+            t_layer = cpu_layer_sample(cfg, cb, ctx, args.rho, args.union, reps=2, warm=1)
+            cpu = {"value": cb / (t_layer * L), "unit": "tok/s", "cores": cpu_threads(), "kind": "port",
+                   "sample": f"oracle (numpy port of the reference path) on one decode layer of the same "
+                             f"workload at B={cb}, median of 2 after 1 warm-up, x {L} layers"}
+        line = {
+            "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_polar / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights N(0,0.02); N(0,1) KV history; hot-neuron router bias)",
+            "config": dict(workload_config(args, cfg), kv_storage_buffers=ring,
+                           kv_aliasing=("none" if ring == L else f"K/V storage aliased over {ring} buffers")),
+            "dense": {"value": dense_value, "ms_per_step": ms_dense / args.steps},
+            "speedup_vs_dense": value / dense_value,
+            "union_density_measured": union_density,
+            "e2e": {"value": toks / (ms_e2e * 1e-3), "unit": "tok/s", "h2d_bytes_per_step": B * 4,
+                    "d2h_bytes_per_step": B * 8, "wall_ms_per_step": wall_e2e / args.steps},
+            "gpu_launches": int(eng.launches_per_step) * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "sha_decode_kernel", "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "peak_kind": peak_kind, "bytes_per_launch": sha_bytes, "us_per_launch": sha_ms * 1e3},
+            "kernels": {"sparse_mlp_us_per_layer": None if mlp_ms is None else mlp_ms * 1e3,
+                        "sparse_mlp_GBps": None if mlp_ms is None else mlp_bytes / (mlp_ms * 1e-3) / 1e9},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

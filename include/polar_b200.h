@@ -112,6 +112,14 @@ int ps_topk_rows(const float* logits, int rows, int cols, int64_t ld, int k,
                  int32_t* idx_out, uint32_t* bitmap, void* stream);
 int ps_threshold_rows(const float* logits, int rows, int cols, int64_t ld, float thr,
                       uint32_t* bitmap, void* stream);
+/* Fused per-row selection + union + compaction (one launch per layer): top-k
+ * (k > 0) or threshold (k <= 0: logit > thr) per row ORed into `bitmap`, then
+ * the last CTA compacts bits [lo, hi) into union_out / count_out exactly as
+ * ps_bitmap_compact does and clears the bitmap.  `ticket`: one int32,
+ * zero-filled before first use (self-resetting). */
+int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr,
+                    uint32_t* bitmap, int* ticket, int lo, int hi, int pad,
+                    int32_t* union_out, int32_t* count_out, void* stream);
 int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width,
                   uint32_t* bitmap, void* stream);
 int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, int pad,
@@ -140,30 +148,34 @@ int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const floa
  *               (+ residual[n, j] if residual != NULL, added after act)
  *   for j < count (count = *count_dev if count_dev else M), n < N;
  *   columns j in [count, M_pad) of out are written as 0.
- *   w_rows bf16 (rows, K) row-major (neuron-major);  x bf16 (N, K) row b at
+ *   w_rows bf16 (w_height, K) row-major (neuron-major);  x bf16 (N, K) row b at
  *   +b*x_ld;  out (N, M_pad) f32/bf16 row n at +n*out_ld.
  *
  * ps_gather_gemm_t ("contraction" form; replaces selective_gemm_t,
  * kernels.py:294-310, and the down-projection of sparse_mlp_forward):
  *   out[n, m] = sum_{j < count} h[n, j] * w_rows[idx[j], m] + bias[m]
  *               (+ residual[n, m] if residual != NULL)
- *   w_rows bf16 (rows, M) row-major;  h bf16 (N, K_pad) row n at +n*h_ld
+ *   w_rows bf16 (w_height, M) row-major;  h bf16 (N, K_pad) row n at +n*h_ld
  *   with K_pad >= count rounded up to 64 and zero beyond count.
  *
- * idx is int32 (NULL = identity), padded to a multiple of 128 entries
- * (ps_bitmap_compact(pad=128) produces this).  Requirements: K % 8 == 0 for
- * the rows form, M % 8 == 0 for the contraction form, 16-byte aligned rows.
+ * idx is int32 (NULL = identity) with ids < w_height.  Operands are moved by
+ * the TMA engine (2-D tiles; sm_100 tile::gather4 for gathered rows), so
+ * rows must be 16-byte aligned: K % 8 == 0 (rows form), M % 8 == 0
+ * (contraction form), x_ld / h_ld % 8 == 0.
  * ws >= ps_gather_gemm_workspace_bytes(...) and zero-filled before first use.
  * ==================================================================== */
+/* debug / tuning hook: per-CTA globaltimer trace (8 x u64 per CTA) and
+ * overrides of the pipeline depth and split-K CTA target (0 = default) */
+void ps_debug_gemm_trace(void* buf, int stages, int target_ctas);
 size_t ps_gather_gemm_workspace_bytes(int N, int M, int K, int splits);
 int ps_gather_gemm_auto_splits(int N, int M, int K);
-int ps_gather_gemm(const void* w_rows, const int32_t* idx, const int32_t* count_dev,
+int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                    const void* x, int64_t x_ld, const float* bias,
                    const float* residual, int64_t residual_ld,
                    int N, int M, int K, int act, int splits,
                    void* out, int64_t out_ld, int out_dtype,
                    void* ws, size_t ws_bytes, void* stream);
-int ps_gather_gemm_t(const void* w_rows, const int32_t* idx, const int32_t* count_dev,
+int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                      const void* h, int64_t h_ld, const float* bias, const float* residual,
                      int64_t residual_ld, int N, int M, int K_max, int splits,
                      void* out, int64_t out_ld, int out_dtype,

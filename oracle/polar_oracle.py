@@ -491,12 +491,15 @@ def random_model(layers, model_dim, ffn_dim, heads, kv_heads, vocab, max_seq,
 
 def decode_step(model: dict, caches, tokens, *, mode="dense", head_density=1.0,
                 layer0_dense=True, k_table=None, head_routers=None,
-                mlp_routers=None, block_size=64, record=None) -> np.ndarray:
+                mlp_routers=None, block_size=64, record=None, forced=None) -> np.ndarray:
     """engine.py:314-392 -- one batched decode step, returns (B, vocab) f32.
 
     ``k_table`` maps layer -> neuron budget (calibration.py:64-68); routers
     are dicts from ``init_*_router``.  ``record`` (optional dict) receives
     the per-layer selections so tests can compare them bit-exactly.
+    ``forced`` (optional dict with per-layer "heads" / "union" lists, keyed
+    by layer) replaces the router selections -- used to check a device step
+    against this oracle given the device's own (bit-exactly checked) picks.
     """
     cfg = model["config"]
     d, H, H_kv = cfg["model_dim"], cfg["heads"], cfg["kv_heads"]
@@ -519,9 +522,12 @@ def decode_step(model: dict, caches, tokens, *, mode="dense", head_density=1.0,
         sparse_heads = (mode == "polar" and not (ell == 0 and layer0_dense)
                         and head_density < 1.0)
         if sparse_heads:
-            r = head_routers[ell]
-            logits = head_router_forward(r["w"], r["b"], h1)
-            sel = topk_indices_rows(logits, head_budget(head_density, H_kv))
+            if forced is not None and ell in forced.get("heads", {}):
+                sel = np.asarray(forced["heads"][ell], np.int64)
+            else:
+                r = head_routers[ell]
+                logits = head_router_forward(r["w"], r["b"], h1)
+                sel = topk_indices_rows(logits, head_budget(head_density, H_kv))
         else:
             sel = np.tile(np.arange(H_kv, dtype=np.int64), (batch, 1))
         if record is not None:
@@ -535,6 +541,8 @@ def decode_step(model: dict, caches, tokens, *, mode="dense", head_density=1.0,
             logits = mlp_router_forward(r["w_in"], r["b_in"], r["w_out"], r["b_out"], h2)
             rows = topk_indices_rows(logits, k_ell)
             union = union_neuron_indices(list(rows))
+            if forced is not None and ell in forced.get("union", {}):
+                union = np.asarray(forced["union"][ell], np.int64)
             if record is not None:
                 record.setdefault("union", []).append(union)
             mlp = sparse_mlp_forward(h2[:, None, :], lw["mlp_w1"], lw["mlp_b1"],

@@ -127,6 +127,29 @@ PS_DEV uint64_t policy_evict_first() {
   return p;
 }
 
+// ---------------------------------------------------------------- TMA tensor loads
+PS_DEV void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+
+// 2-D tiled box load (swizzle from the tensor map), completion on `bar`.
+PS_DEV void tma_load_2d(void* smem_dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// sm_100 row gather: 4 rows (r0..r3) x box-width columns starting at c0.
+PS_DEV void tma_gather4(void* smem_dst, const void* tmap, int c0, int r0, int r1, int r2, int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 // 16-byte async copy; src_bytes < 16 zero-fills the remainder (0 = all zero).
 PS_DEV void cp_async16(void* smem_dst, const void* gmem_src, uint32_t src_bytes) {
@@ -207,6 +230,17 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, int a_mn, i
          | ((uint32_t)b_mn << 16)        // b major
          | ((uint32_t)(N >> 3) << 17)    // N >> 3
          | ((uint32_t)(M >> 4) << 24);   // M >> 4
+}
+
+// fire-and-forget f32 reduction into global memory (REDG, no return value)
+PS_DEV void red_add_f32(float* addr, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+
+PS_DEV void red_add_v4(float* addr, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
 }
 
 // ---------------------------------------------------------------- misc

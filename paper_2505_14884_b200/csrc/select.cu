@@ -46,96 +46,214 @@ PS_DEV int block_excl_scan(int v, int* s_warp, int* total) {
 }
 
 constexpr int kTopkThreads = 512;
+constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kTopkSmemCols = 49152;  // rows up to this width are staged in shared memory
 
-// One CTA per row: 4-pass 8-bit radix select of the k-th largest key, then
-// an index-order pass that keeps every key above it and the lowest-index
-// ties up to k (exactly the stable-argsort rule).
-__global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const float* __restrict__ logits, int cols,
-                                                                 int64_t ld, int k, int32_t* __restrict__ idx_out,
-                                                                 uint32_t* __restrict__ bitmap) {
-  __shared__ int hist[256];
+struct TopkParams {
+  const float* logits;
+  int rows, cols;
+  int64_t ld;
+  int k;            // > 0: top-k per row; <= 0: threshold selection (logit > thr)
+  float thr;
+  int32_t* idx_out;  // (rows, k) ascending ids, or NULL
+  uint32_t* bitmap;  // union bitmap (atomic OR), or NULL
+  // fused union compaction by the last CTA (ticket != NULL)
+  int* ticket;
+  int lo, hi, pad;
+  int32_t* union_out;
+  int32_t* count_out;
+};
+
+// Last-CTA compaction of bitmap bits in [lo, hi) -> ascending ids - lo;
+// clears the whole bitmap.  Called by every thread of one CTA.
+template <int NT>
+PS_DEV void compact_bitmap(uint32_t* bitmap, int width, int lo, int hi, int pad, int32_t* out, int32_t* count,
+                           int* s_warp) {
+  const int words = (width + 31) >> 5;
+  const int wlo = lo >> 5, whi = (hi + 31) >> 5;
+  const int nw = whi - wlo;
+  const int per = (nw + NT - 1) / NT;
+  const int w0 = wlo + min(nw, (int)threadIdx.x * per), w1 = wlo + min(nw, (int)(threadIdx.x + 1) * per);
+  auto word = [&](int w) {
+    uint32_t bits = __ldcg(bitmap + w);
+    const int top = hi - (w << 5);
+    if (top < 32) bits &= (top <= 0) ? 0u : ((1u << top) - 1u);
+    return bits;
+  };
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(word(w));
+  int total;
+  int pos = block_excl_scan<NT>(cnt, s_warp, &total);
+  for (int w = w0; w < w1; ++w) {
+    uint32_t bits = word(w);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      out[pos++] = (w << 5) + b - lo;
+    }
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < words; w += NT) bitmap[w] = 0u;
+  if (threadIdx.x == 0) *count = total;
+  if (pad > 1) {
+    const int padded = (total + pad - 1) / pad * pad;
+    __syncthreads();
+    const int32_t last = total > 0 ? out[total - 1] : 0;
+    for (int i = total + threadIdx.x; i < padded; i += NT) out[i] = last;
+  }
+}
+
+// One CTA per row.  Top-k: 3-pass (12/10/10-bit) radix select of the k-th
+// largest key over keys staged in shared memory, then ONE index-order pass in which each
+// warp owns a contiguous segment and ranks its elements with ballots: keep
+// every key above the k-th and the lowest-index ties up to k (exactly the
+// stable-argsort rule).  Threshold mode keeps logit > thr.  Each 32-id word
+// of the selection is ORed into the union bitmap once, by one lane.
+__global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int* hist = reinterpret_cast<int*>(smem);                              // [4096] radix histogram
+  uint32_t* keys = reinterpret_cast<uint32_t*>(hist + 4096);              // [cols] if staged
   __shared__ int s_warp[32];
+  __shared__ int s_eq[kTopkWarps], s_gt[kTopkWarps];
   __shared__ uint32_t s_prefix;
-  __shared__ int s_remaining;
-  const int row = blockIdx.x;
-  const float* x = logits + (size_t)row * ld;
-  const int tid = threadIdx.x;
+  __shared__ int s_remaining, s_last;
+  const int row = blockIdx.x, cols = p.cols;
+  const float* x = p.logits + (size_t)row * p.ld;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool threshold = p.k <= 0;
+  const bool staged = !threshold && cols <= kTopkSmemCols;
+  auto key_at = [&](int i) -> uint32_t { return staged ? keys[i] : order_key(__ldg(x + i)); };
 
-  uint32_t prefix = 0, mask = 0;
-  int remaining = k;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = tid; i < 256; i += kTopkThreads) hist[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < cols; i += kTopkThreads) {
-      const uint32_t u = order_key(__ldg(x + i));
-      if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1);
-    }
-    __syncthreads();
-    if (tid < 32) {
-      int loc[8], lsum = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        loc[j] = hist[tid * 8 + j];
-        lsum += loc[j];
+  uint32_t prefix = 0;
+  int remaining = 0;
+  if (!threshold) {
+    if (staged)
+      for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(__ldg(x + i));
+    // three radix passes over (12, 10, 10) key bits; only keys matching the
+    // prefix found so far touch the histogram, so after the first pass
+    // (where the exponent clustering of real logits spreads over ~10^2
+    // bins) almost no atomics are issued
+    remaining = p.k;
+    uint32_t mask = 0;
+    const int shifts[3] = {20, 10, 0};
+    const int nbins[3] = {4096, 1024, 1024};
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+      const int shift = shifts[pass], bins = nbins[pass];
+      for (int i = tid; i < bins; i += kTopkThreads) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < cols; i += kTopkThreads) {
+        const uint32_t u = key_at(i);
+        if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & (uint32_t)(bins - 1)], 1);
       }
-      int incl = lsum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += y;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      int cum = total - incl;  // count in bins above this lane's range
-#pragma unroll
-      for (int j = 7; j >= 0; --j) {
-        if (cum < remaining && cum + loc[j] >= remaining) {
-          s_prefix = prefix | ((uint32_t)(tid * 8 + j) << shift);
-          s_remaining = remaining - cum;
+      __syncthreads();
+      // descending scan: thread t owns bins [bins - (t+1)*per, bins - t*per)
+      const int per = bins / kTopkThreads;  // 8 or 2
+      const int hi = bins - tid * per;
+      int loc = 0;
+      for (int j = 1; j <= per; ++j) loc += hist[hi - j];
+      const int above = block_excl_scan<kTopkThreads>(loc, s_warp, nullptr);
+      if (above < remaining && above + loc >= remaining) {
+        int cum = above;
+        for (int j = 1; j <= per; ++j) {
+          const int c = hist[hi - j];
+          if (cum + c >= remaining) {
+            s_prefix = prefix | ((uint32_t)(hi - j) << shift);
+            s_remaining = remaining - cum;
+            break;
+          }
+          cum += c;
         }
-        cum += loc[j];
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      remaining = s_remaining;
+      mask |= (uint32_t)(bins - 1) << shift;
+      __syncthreads();
+    }
+  }
+
+  // ---- index-order selection: warp-contiguous segments (multiples of 32)
+  const int seg = (cols + kTopkThreads - 1) / kTopkThreads * 32;
+  const int sbeg = warp * seg, send = min(cols, sbeg + seg);
+  auto classify = [&](int e, bool& gt, bool& eq) {
+    gt = eq = false;
+    if (e < send) {
+      if (threshold) {
+        gt = __ldg(x + e) > p.thr;
+      } else {
+        const uint32_t u = key_at(e);
+        gt = u > prefix;
+        eq = u == prefix;
       }
     }
-    __syncthreads();
-    prefix = s_prefix;
-    remaining = s_remaining;
-    mask |= 255u << shift;
+  };
+  int n_eq = 0, n_gt = 0;
+  if (!threshold || p.idx_out) {
+    for (int e0 = sbeg; e0 < send; e0 += 32) {
+      bool gt, eq;
+      classify(e0 + lane, gt, eq);
+      n_gt += __popc(__ballot_sync(0xffffffffu, gt));
+      n_eq += __popc(__ballot_sync(0xffffffffu, eq));
+    }
+    if (lane == 0) {
+      s_eq[warp] = n_eq;
+      s_gt[warp] = n_gt;
+    }
     __syncthreads();
   }
-  // prefix = k-th largest key; take all keys > prefix and the first
-  // `remaining` (lowest-index) keys == prefix.
-  const int per = (cols + kTopkThreads - 1) / kTopkThreads;
-  const int c0 = min(cols, tid * per), c1 = min(cols, c0 + per);
-  int n_eq = 0;
-  for (int i = c0; i < c1; ++i) n_eq += (order_key(__ldg(x + i)) == prefix);
-  const int eq_before = block_excl_scan<kTopkThreads>(n_eq, s_warp, nullptr);
-  int n_sel = 0, eq_seen = eq_before;
-  for (int i = c0; i < c1; ++i) {
-    const uint32_t u = order_key(__ldg(x + i));
-    if (u > prefix) ++n_sel;
-    else if (u == prefix) n_sel += (eq_seen++ < remaining);
+  int eq_before = 0, gt_before = 0;
+  if (!threshold || p.idx_out)
+    for (int w = 0; w < warp; ++w) {
+      eq_before += s_eq[w];
+      gt_before += s_gt[w];
+    }
+  int pos = gt_before + (threshold ? 0 : min(eq_before, remaining));
+  int eq_run = eq_before;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int e0 = sbeg; e0 < send; e0 += 32) {
+    bool gt, eq;
+    classify(e0 + lane, gt, eq);
+    const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+    const bool take = gt || (eq && (eq_run + __popc(beq & lt)) < remaining);
+    const uint32_t bt = __ballot_sync(0xffffffffu, take);
+    eq_run += __popc(beq);
+    if (take && p.idx_out) p.idx_out[(size_t)row * p.k + pos + __popc(bt & lt)] = e0 + lane;
+    pos += __popc(bt);
+    if (p.bitmap && lane == 0 && bt) atomicOr(p.bitmap + (e0 >> 5), bt);
   }
-  int pos = block_excl_scan<kTopkThreads>(n_sel, s_warp, nullptr);
-  eq_seen = eq_before;
-  for (int i = c0; i < c1; ++i) {
-    const uint32_t u = order_key(__ldg(x + i));
-    bool take = false;
-    if (u > prefix) take = true;
-    else if (u == prefix) take = (eq_seen++ < remaining);
-    if (take) {
-      if (idx_out) idx_out[(size_t)row * k + pos] = i;
-      if (bitmap) atomicOr(bitmap + (i >> 5), 1u << (i & 31));
-      ++pos;
+
+  // ---- fused union compaction by the last CTA
+  if (p.ticket) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(p.ticket, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      compact_bitmap<kTopkThreads>(p.bitmap, cols, p.lo, p.hi, p.pad, p.union_out, p.count_out, s_warp);
+      if (tid == 0) *p.ticket = 0;
     }
   }
 }
 
-__global__ void threshold_rows_kernel(const float* __restrict__ logits, int rows, int cols, int64_t ld, float thr,
-                                      uint32_t* __restrict__ bitmap) {
-  const int64_t total = (int64_t)rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / cols), c = (int)(e - (int64_t)r * cols);
-    if (__ldg(logits + (size_t)r * ld + c) > thr) atomicOr(bitmap + (c >> 5), 1u << (c & 31));
+size_t topk_smem(int cols, bool threshold) {
+  size_t b = (size_t)4096 * 4;
+  if (!threshold && cols <= kTopkSmemCols) b += (size_t)cols * 4;
+  return b;
+}
+
+int launch_topk(const TopkParams& prm, cudaStream_t st) {
+  const size_t smem = topk_smem(prm.cols, prm.k <= 0);
+  static int configured = 0;
+  if (!configured) {
+    if (cudaFuncSetAttribute(topk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) !=
+        cudaSuccess)
+      return PS_ERR_CUDA;
+    configured = 1;
   }
+  topk_rows_kernel<<<prm.rows, kTopkThreads, smem, st>>>(prm);
+  return launch_status();
 }
 
 __global__ void union_rows_kernel(const int32_t* __restrict__ ids, int n, int width, uint32_t* __restrict__ bitmap) {
@@ -195,7 +313,7 @@ __global__ void __launch_bounds__(kCompactThreads) bitmap_compact_kernel(uint32_
 
 // Head router fused with top-k.  R rows per CTA share each 16-byte W^T load.
 constexpr int kHrThreads = 256;
-constexpr int kHrRows = 4;
+constexpr int kHrRows = 1;
 constexpr int kHrMaxHeads = 256;
 
 __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
@@ -273,19 +391,32 @@ extern "C" int ps_topk_rows(const float* logits, int rows, int cols, int64_t ld,
                             uint32_t* bitmap, void* stream) {
   if (rows < 1 || cols < 1 || ld < cols || k < 1 || k > cols || !logits) return PS_ERR_VALUE;
   if (!idx_out && !bitmap) return PS_ERR_VALUE;
-  topk_rows_kernel<<<rows, kTopkThreads, 0, static_cast<cudaStream_t>(stream)>>>(logits, cols, ld, k, idx_out,
-                                                                                 bitmap);
-  return launch_status();
+  TopkParams prm{};
+  prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k;
+  prm.idx_out = idx_out; prm.bitmap = bitmap;
+  return launch_topk(prm, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int ps_threshold_rows(const float* logits, int rows, int cols, int64_t ld, float thr, uint32_t* bitmap,
                                  void* stream) {
   if (rows < 1 || cols < 1 || ld < cols || !logits || !bitmap) return PS_ERR_VALUE;
-  const int64_t total = (int64_t)rows * cols;
-  int grid = (int)((total + 255) / 256);
-  if (grid > 4 * 148 * 8) grid = 4 * 148 * 8;
-  threshold_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(logits, rows, cols, ld, thr, bitmap);
-  return launch_status();
+  TopkParams prm{};
+  prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = 0; prm.thr = thr;
+  prm.bitmap = bitmap;
+  return launch_topk(prm, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr,
+                               uint32_t* bitmap, int* ticket, int lo, int hi, int pad, int32_t* union_out,
+                               int32_t* count_out, void* stream) {
+  if (rows < 1 || cols < 1 || ld < cols || k > cols || !logits || !bitmap || !ticket || !union_out || !count_out)
+    return PS_ERR_VALUE;
+  if (lo < 0 || lo % 32 || hi > cols || hi <= lo || pad < 1) return PS_ERR_VALUE;
+  TopkParams prm{};
+  prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k > 0 ? k : 0; prm.thr = thr;
+  prm.bitmap = bitmap; prm.ticket = ticket; prm.lo = lo; prm.hi = hi; prm.pad = pad;
+  prm.union_out = union_out; prm.count_out = count_out;
+  return launch_topk(prm, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width, uint32_t* bitmap, void* stream) {

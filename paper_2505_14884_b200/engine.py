@@ -85,11 +85,14 @@ class DecodeEngine:
     """
 
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
-                 head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None):
+                 head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
+                 caches=None, dense_backend: str = "cublas"):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
         self.model, self.cfg, self.B, self.policy = model, cfg, batch, policy
+        self.dense_backend = check_choice(dense_backend, ("cublas", "native"), "dense_backend")
+        self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
         self.tp = tp
         dev = model.device
@@ -123,9 +126,14 @@ class DecodeEngine:
         # KV caches (optionally aliased storage)
         ring = cfg.layers if kv_ring is None else max(1, min(kv_ring, cfg.layers))
         self.kv_ring = ring
-        base = [KVCache(batch, self.Hkv_loc, capacity, d_h, device=dev) for _ in range(ring)]
         self.caches = []
-        for ell in range(cfg.layers):
+        if caches is not None:  # share another engine's caches (e.g. dense vs polar bench)
+            if len(caches) != cfg.layers:
+                raise ValueError("caches must hold one KVCache per layer")
+            self.caches = list(caches)
+            ring = 0
+        base = [KVCache(batch, self.Hkv_loc, capacity, d_h, device=dev) for _ in range(ring)]
+        for ell in range(cfg.layers if ring else 0):
             c = base[ell % ring]
             if ell >= ring:
                 alias = KVCache.__new__(KVCache)
@@ -157,6 +165,7 @@ class DecodeEngine:
             self.r_hid = torch.zeros(batch, h_r, dtype=bf, device=dev)
             self.r_logits = torch.zeros(batch, D, dtype=f32, device=dev)
             self.bitmap = torch.zeros((D + 31) // 32, dtype=torch.int32, device=dev)
+            self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
             self.union_idx = torch.zeros(_round_up(D, ROW_PAD), dtype=torch.int32, device=dev)
             self.union_count = torch.zeros(1, dtype=torch.int32, device=dev)
             self.union_counts = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
@@ -195,6 +204,58 @@ class DecodeEngine:
         if self.tp is not None:
             self.tp.all_reduce(t)
 
+    # ------------------------------------------------------------------ dense glue
+    # Plain dense projections (QKV, O, router layers, dense MLP, LM head) run
+    # on cuBLAS by default ("plain library GEMMs", identical in dense and
+    # polar modes); dense_backend="native" routes them through the tcgen05
+    # gathered-GEMM kernel with identity indices instead.
+    def _bf(self, t: torch.Tensor) -> torch.Tensor:
+        key = ("bf", t.data_ptr())
+        c = self._cache.get(key)
+        if c is None:
+            c = t.to(torch.bfloat16)
+            self._cache[key] = c
+        return c
+
+    def _scratch(self, name, shape, dtype):
+        key = ("scr", name)
+        t = self._cache.get(key)
+        if t is None or tuple(t.shape) != tuple(shape):
+            t = torch.empty(shape, dtype=dtype, device=self.device)
+            self._cache[key] = t
+        return t
+
+    def _linear_bf16(self, x2d, w_t, bias, out, act_relu=False, tag="gg"):
+        """out (bf16) = act(x w^T + bias)."""
+        if self.dense_backend == "cublas":
+            if bias is not None:
+                torch.addmm(self._bf(bias), x2d, w_t.t(), out=out)
+            else:
+                torch.mm(x2d, w_t.t(), out=out)
+            if act_relu:
+                out.relu_()
+            return 0
+        gather_gemm_into(w_t, None, None, x2d, x2d.stride(0), bias, x2d.shape[0], w_t.shape[0], x2d.shape[1],
+                         _lib.PS_ACT_RELU if act_relu else _lib.PS_ACT_NONE, out, out.stride(0), tag=tag)
+        return 1
+
+    def _linear_f32(self, x2d, w_t, bias, out, residual=False, tag="gg"):
+        """out (f32) = x w^T + bias (+ out if residual)."""
+        if self.dense_backend == "cublas":
+            if residual:
+                tmp = self._scratch(tag, out.shape, torch.float32)
+                torch.mm(x2d, w_t.t(), out_dtype=torch.float32, out=tmp)
+                out.add_(tmp)
+            else:
+                torch.mm(x2d, w_t.t(), out_dtype=torch.float32, out=out)
+            if bias is not None:
+                out.add_(bias)
+            return 0
+        gather_gemm_into(w_t, None, None, x2d, x2d.stride(0), bias, x2d.shape[0], w_t.shape[0], x2d.shape[1],
+                         _lib.PS_ACT_NONE, out, out.stride(0), residual=out if residual else None,
+                         res_ld=out.stride(0), tag=tag)
+        return 1
+
     def step_launches(self) -> int:
         """Enqueue one decode step on the current stream; returns the number
         of libpolar_b200 kernel launches enqueued."""
@@ -211,14 +272,14 @@ class DecodeEngine:
             c = self.caches[ell]
             _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(lw.ln1_g), _lib.ptr(lw.ln1_b), B, d,
                                       _lib.ptr(self.h), d, st), "ps_layernorm")
-            gather_gemm_into(lw.w_qkv_t, None, None, self.h, d, lw.b_qkv, B, qkv_w, d, _lib.PS_ACT_NONE,
-                             self.qkv, qkv_w, tag="gg_qkv")
+            n += 1
+            n += self._linear_bf16(self.h, lw.w_qkv_t, lw.b_qkv, self.qkv, tag="gg_qkv")
             kq = self.qkv[:, self.d_loc:]
             vq = self.qkv[:, self.d_loc + self.dk_loc:]
             _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths), _lib.ptr(kq),
                                       _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity, cfg.head_dim,
                                       _lib.ptr(c._err), st), "ps_kv_append")
-            n += 3
+            n += 1
             k_h = self.k_heads[ell]
             if k_h:
                 sel = self.sel[:, :k_h]
@@ -238,46 +299,73 @@ class DecodeEngine:
                             group_base=self.group_base, max_len_hint=int(c.host_lengths.max()) + 1)
             n += 1
             if self.tp is None:
-                gather_gemm_into(lw.w_o_t, None, None, self.attn, self.d_loc, lw.b_o, B, d, self.d_loc,
-                                 _lib.PS_ACT_NONE, self.x, d, residual=self.x, res_ld=d, tag="gg_o")
+                n += self._linear_f32(self.attn, lw.w_o_t, lw.b_o, self.x, residual=True, tag="gg_o")
             else:
-                self.tp.o_proj(self, lw)
-            n += 1
+                n += self.tp.o_proj(self, lw)
             _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(lw.ln2_g), _lib.ptr(lw.ln2_b), B, d,
                                       _lib.ptr(self.h), d, st), "ps_layernorm")
             n += 1
             if self.sparse_mlp:
-                self.mlp_routers[ell].logits_into(self.h, self.r_hid, self.r_logits)
-                _lib.check(L.ps_topk_rows(_lib.ptr(self.r_logits), B, cfg.ffn_dim, cfg.ffn_dim, self.k_mlp[ell],
-                                          None, _lib.ptr(self.bitmap), st), "ps_topk_rows")
+                r = self.mlp_routers[ell]
+                if self.dense_backend == "cublas":
+                    n += self._linear_bf16(self.h, r.w_in_t, r.b_in, self.r_hid, act_relu=True)
+                    n += self._linear_f32(self.r_hid, r.w_out_t, r.b_out, self.r_logits)
+                else:
+                    r.logits_into(self.h, self.r_hid, self.r_logits)
+                    n += 2
                 lo, hi = (0, cfg.ffn_dim) if self.tp is None else self.tp.ffn_range
-                _lib.check(L.ps_bitmap_compact(_lib.ptr(self.bitmap), cfg.ffn_dim, lo, hi, ROW_PAD,
-                                               _lib.ptr(self.union_idx), _lib.ptr(self.union_count), st),
-                           "ps_bitmap_compact")
-                n += 4
-                idx, cnt = self.union_idx, self.union_count
+                _lib.check(L.ps_select_union(_lib.ptr(self.r_logits), B, cfg.ffn_dim, cfg.ffn_dim,
+                                             self.k_mlp[ell], 0.0, _lib.ptr(self.bitmap), _lib.ptr(self.ticket),
+                                             lo, hi, ROW_PAD, _lib.ptr(self.union_idx),
+                                             _lib.ptr(self.union_count), st), "ps_select_union")
+                n += 1
                 if self.record is not None:
                     self.record.setdefault("mlp_logits", []).append(self.r_logits.clone())
-                    self.record.setdefault("union", []).append(self.union_idx[: int(cnt.item())].clone())
-            else:
-                idx = cnt = None
-            resid = self.x if self.tp is None else None
-            if self.tp is None:
-                if cfg.activation == "swiglu":
-                    swiglu_into(lw.mlp, self.h, self.gu, self.hidden, self.x, residual=self.x)
-                    n += 3
-                else:
-                    mlp_into(lw.mlp, self.h, idx, cnt, self.hidden, self.x, residual=resid)
+                    self.record.setdefault("union", []).append(
+                        self.union_idx[: int(self.union_count.item())].clone())
+                if self.tp is None:
+                    mlp_into(lw.mlp, self.h, self.union_idx, self.union_count, self.hidden, self.x,
+                             residual=self.x)
                     n += 2
+                else:
+                    n += self.tp.mlp(self, lw, self.union_idx, self.union_count)
+            elif self.tp is not None:
+                n += self.tp.mlp(self, lw, None, None)
+            elif cfg.activation == "swiglu":
+                mk = lw.mlp
+                if self.dense_backend == "cublas":
+                    torch.mm(self.h, mk.gate_up().t(), out=self.gu)
+                    _lib.call("ps_swiglu", _lib.ptr(self.gu), self.gu.stride(0), B, mk.D, _lib.ptr(self.hidden),
+                              self.hidden.stride(0), st)
+                    n += 1
+                    self._dense_down(mk, self.hidden[:, :mk.D])
+                else:
+                    swiglu_into(mk, self.h, self.gu, self.hidden, self.x, residual=self.x)
+                    n += 3
             else:
-                n += self.tp.mlp(self, lw, idx, cnt)
+                mk = lw.mlp
+                if self.dense_backend == "cublas":
+                    hid = self._scratch("hid", (B, mk.D), torch.bfloat16)
+                    n += self._linear_bf16(self.h, mk.w1t, mk.b1, hid, act_relu=True)
+                    self._dense_down(mk, hid)
+                else:
+                    mlp_into(mk, self.h, None, None, self.hidden, self.x, residual=self.x)
+                    n += 2
         _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(m.lnf_g), _lib.ptr(m.lnf_b), B, d,
                                   _lib.ptr(self.h), d, st), "ps_layernorm")
-        gather_gemm_into(m.unembed_t, None, None, self.h, d, None, B, cfg.vocab, d, _lib.PS_ACT_NONE,
-                         self.logits, cfg.vocab, tag="gg_lm")
-        n += 2
+        n += 1
+        n += self._linear_f32(self.h, m.unembed_t, None, self.logits, tag="gg_lm")
         torch.argmax(self.logits, dim=1, out=self.next_tokens)
         return n
+
+    def _dense_down(self, mk, hid) -> None:
+        """x += hid @ W2 + b2 with W2^T stored neuron-major (D, d): a plain
+        (B, D) x (D, d) cuBLAS GEMM on the packed rows."""
+        tmp = self._scratch("down", self.x.shape, torch.float32)
+        torch.mm(hid, mk.w2t, out_dtype=torch.float32, out=tmp)
+        self.x.add_(tmp)
+        if mk.b2 is not None:
+            self.x.add_(mk.b2)
 
     def sel_bufs(self, k: int) -> torch.Tensor:
         key = f"_sel_{k}"

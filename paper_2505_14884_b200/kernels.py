@@ -250,7 +250,8 @@ def gather_gemm_into(w_rows, idx, count, x, x_ld, bias, N, M, K, act, out, out_l
         splits = lib.ps_gather_gemm_auto_splits(N, M, K)
     ws = _ws.get(tag, lib.ps_gather_gemm_workspace_bytes(N, M, K, splits), out.device)
     dt = _lib.PS_DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.PS_DTYPE_F32
-    _lib.call("ps_gather_gemm", _lib.ptr(w_rows), _lib.ptr(idx), _lib.ptr(count), _lib.ptr(x), int(x_ld),
+    _lib.call("ps_gather_gemm", _lib.ptr(w_rows), w_rows.shape[0], _lib.ptr(idx), _lib.ptr(count), _lib.ptr(x),
+              int(x_ld),
               _lib.ptr(bias), _lib.ptr(residual), int(res_ld), N, M, K, act, splits, _lib.ptr(out),
               int(out_ld), dt, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
 
@@ -263,7 +264,8 @@ def gather_gemm_t_into(w_rows, idx, count, h, h_ld, bias, N, M, K_max, out, out_
         splits = lib.ps_gather_gemm_auto_splits(N, M, K_max)
     ws = _ws.get(tag, lib.ps_gather_gemm_workspace_bytes(N, M, K_max, splits), out.device)
     dt = _lib.PS_DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.PS_DTYPE_F32
-    _lib.call("ps_gather_gemm_t", _lib.ptr(w_rows), _lib.ptr(idx), _lib.ptr(count), _lib.ptr(h), int(h_ld),
+    _lib.call("ps_gather_gemm_t", _lib.ptr(w_rows), w_rows.shape[0], _lib.ptr(idx), _lib.ptr(count), _lib.ptr(h),
+              int(h_ld),
               _lib.ptr(bias), _lib.ptr(residual), int(res_ld), N, M, K_max, splits, _lib.ptr(out),
               int(out_ld), dt, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
 

@@ -119,6 +119,30 @@ class MlpRouter:
         self.b_out = f32(b_out).to(dev)
 
     @classmethod
+    def random_device(cls, d_model: int, ffn_dim: int, hidden_dim: int | None = None, seed: int = 0,
+                      device=None, hot=None, hot_bias: float = 20.0) -> "MlpRouter":
+        """Router drawn on the device with the reference's distribution
+        (N(0, sqrt(2/d)), N(0, sqrt(2/h)), zero biases) -- for production
+        shapes where host-side init is slow.  ``hot`` (neuron ids) adds
+        ``hot_bias`` to their output bias: the controlled "hot neuron" union
+        density of SURVEY.md §7 / analysis.py:124-140 (every token's top-k
+        then covers the hot set, so |S|/D is set by the caller)."""
+        obj = cls.__new__(cls)
+        h = hidden_dim if hidden_dim is not None else min(1024, 4 * d_model)
+        obj.d_model, obj.ffn_dim, obj.hidden_dim_, obj.seed = d_model, ffn_dim, h, seed
+        dev = torch.device(device or default_device())
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        obj.w_in_t = (torch.randn(h, d_model, device=dev, generator=gen) * math.sqrt(2.0 / d_model)).to(
+            torch.bfloat16)
+        obj.w_out_t = (torch.randn(ffn_dim, h, device=dev, generator=gen) * math.sqrt(2.0 / h)).to(torch.bfloat16)
+        obj.b_in = torch.zeros(h, device=dev)
+        obj.b_out = torch.zeros(ffn_dim, device=dev)
+        if hot is not None:
+            obj.b_out[torch.as_tensor(np.asarray(hot), device=dev, dtype=torch.long)] += hot_bias
+        return obj
+
+    @classmethod
     def from_reference(cls, router, device=None) -> "MlpRouter":
         return cls(router.w_in_.shape[0], router.w_out_.shape[1], router.w_in_.shape[1],
                    getattr(router, "seed", 0), device,
@@ -174,19 +198,15 @@ def union_from_logits(logits: torch.Tensor, k: int | None = None, threshold: flo
     rows, width = logits.shape
     logits = logits.contiguous().float()
     dev = logits.device
+    if k is not None and not 1 <= k <= width:
+        raise ValueError(f"k must be in [1, {width}], got {k}")
     bitmap = _ws.get("union_bitmap", ((width + 31) // 32) * 4, dev)
-    if k is not None:
-        if not 1 <= k <= width:
-            raise ValueError(f"k must be in [1, {width}], got {k}")
-        _lib.call("ps_topk_rows", _lib.ptr(logits), rows, width, width, int(k), None, _lib.ptr(bitmap),
-                  _lib.stream_ptr())
-    else:
-        _lib.call("ps_threshold_rows", _lib.ptr(logits), rows, width, width, float(threshold or 0.0),
-                  _lib.ptr(bitmap), _lib.stream_ptr())
+    ticket = _ws.get("union_ticket", 4, dev)
     buf = torch.empty(_round_up(width, ROW_PAD), dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.call("ps_bitmap_compact", _lib.ptr(bitmap), width, 0, width, ROW_PAD, _lib.ptr(buf), _lib.ptr(cnt),
-              _lib.stream_ptr())
+    _lib.call("ps_select_union", _lib.ptr(logits), rows, width, width, int(k) if k is not None else 0,
+              float(threshold or 0.0), _lib.ptr(bitmap), _lib.ptr(ticket), 0, width, ROW_PAD, _lib.ptr(buf),
+              _lib.ptr(cnt), _lib.stream_ptr())
     return NeuronIndexTensor(layer, buf, cnt)
 
 

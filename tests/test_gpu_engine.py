@@ -4,7 +4,7 @@ tiny OPT-style decoder, 2 layers, d=256, 8 heads, ReLU MLP, batch 8, ctx 256.
 * head and neuron selections are bit-exact to the reference rule applied
   to the GPU router's own logits (top-k / union given identical logits);
 * logits match the reference's (golden) within bf16 tolerance;
-* the CUDA-graph replay is bitwise identical to the eager step.
+* the CUDA-graph replay matches the eager step (to f32 rounding).
 """
 
 import numpy as np
@@ -71,15 +71,25 @@ def test_polar_step_selection_and_logits(golden, tag, kv_heads):
         ml = rec["mlp_logits"][ell].cpu().numpy()
         ref_union = po.union_neuron_indices(list(po.topk_indices_rows(ml, 128)))
         assert np.array_equal(rec["union"][ell].cpu().numpy(), ref_union)
-    # router logits themselves vs the reference routers (f64 there, bf16 here)
-    same = np.array_equal(rec["heads"][0].cpu().numpy(), golden[f"dec_{tag}_polar_heads_1"])
-    u_same = all(np.array_equal(rec["union"][e].cpu().numpy(), golden[f"dec_{tag}_polar_union_{e}"])
-                 for e in range(2))
-    ref = golden[f"dec_{tag}_polar_logits"]
-    if same and u_same:
-        assert _rel(logits, ref) <= 2e-2
-    else:  # a near-tie flipped under bf16 router weights: still close overall
-        assert _rel(logits, ref) <= 1e-1
+    # logits vs the oracle decode step run with the device's (checked) selections
+    host = po.random_model(2, 256, 1024, 8, kv_heads, 512, 288, seed=21)
+    rng = np.random.default_rng(22)
+    caches = []
+    for _ in range(2):
+        c = po.KVCache(8, kv_heads, 288, 32)
+        c.fill_random(rng, 256)
+        caches.append(c)
+    forced = {"heads": {1: rec["heads"][0].cpu().numpy()},
+              "union": {e: rec["union"][e].cpu().numpy() for e in range(2)}}
+    ref = po.decode_step(host, caches, tokens, mode="polar", head_density=0.5, k_table={0: 128, 1: 128},
+                         head_routers=[None, None], mlp_routers=[po.init_mlp_router(256, 1024, seed=30 + e)
+                                                                 for e in range(2)],
+                         forced=forced)
+    assert _rel(logits, ref) <= 2e-2
+    # when the bf16 routers pick the reference's exact sets, match its golden logits too
+    if np.array_equal(rec["heads"][0].cpu().numpy(), golden[f"dec_{tag}_polar_heads_1"]) and all(
+            np.array_equal(rec["union"][e].cpu().numpy(), golden[f"dec_{tag}_polar_union_{e}"]) for e in range(2)):
+        assert _rel(logits, golden[f"dec_{tag}_polar_logits"]) <= 2e-2
 
 
 @pytest.mark.parametrize("mode", ["dense", "polar"])
@@ -90,7 +100,8 @@ def test_graph_replay_equals_eager(mode):
     for _ in range(3):
         la = eng_a.step(tokens).clone()
         lb = eng_b.step(tokens).clone()
-        assert torch.equal(la, lb)
+        # shared GEMM tiles are reduced with f32 atomics: equal up to f32 rounding
+        assert torch.allclose(la, lb, rtol=1e-4, atol=1e-5)
     assert np.array_equal(eng_a.host_lengths, eng_b.host_lengths)
     assert eng_b.caches[1].lengths.cpu().tolist() == [259] * 8
 
