@@ -167,6 +167,9 @@ int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const floa
 /* debug / tuning hook: per-CTA globaltimer trace (8 x u64 per CTA) and
  * overrides of the pipeline depth and split-K CTA target (0 = default) */
 void ps_debug_gemm_trace(void* buf, int stages, int target_ctas);
+/* A-operand copy engine: 0 = TMA (tile / tile::gather4), 1 = cp.async loader
+ * warps for gathered rows (default), 2 = cp.async loader warps always */
+void ps_debug_gemm_lsu_mode(int mode);
 size_t ps_gather_gemm_workspace_bytes(int N, int M, int K, int splits);
 int ps_gather_gemm_auto_splits(int N, int M, int K);
 int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,

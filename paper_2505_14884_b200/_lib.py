@@ -43,6 +43,7 @@ SIGNATURES = {
     "ps_bitmap_compact": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_head_router_topk": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_debug_gemm_trace": (None, [_vp, _i, _i]),
+    "ps_debug_gemm_lsu_mode": (None, [_i]),
     "ps_gather_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "ps_gather_gemm_auto_splits": (_i, [_i, _i, _i]),
     "ps_gather_gemm": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i,

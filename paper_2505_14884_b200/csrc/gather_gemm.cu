@@ -8,28 +8,26 @@
 //   rows form   (MODE_UP):   out[n, j] = act(sum_k W[idx[j], k] x[n, k] + b[idx[j]]) (+ res)
 //   contraction (MODE_DOWN): out[n, m] = sum_j h[n, j] W[idx[j], m] + b[m] (+ res)
 //
-// Decode GEMMs are weight-streaming (batch N <= 256 << the ~250 flop/byte
-// ridge), so the design goal is every SM streaming weights continuously:
+// Decode GEMMs stream weights (batch N <= 256 << the ~250 flop/byte ridge),
+// so the design goal is every SM streaming weights continuously with short
+// prologue / epilogue tails:
 //   * swap-AB: the UMMA M dimension (128) runs over the weight side (neurons
 //     for UP, output features for DOWN), N over the batch (16..256);
-//   * persistent stream-K: a fixed grid (SMs x 2) splits the total
-//     (tile, 64-wide K block) iteration space evenly ON THE DEVICE, from the
-//     device-resident union size (*count) -- no host sync, graph-capturable,
-//     no idle waves whatever |S| is; CTAs sharing a tile add their partial
-//     sums into an f32 tile accumulator with fire-and-forget global
-//     reductions, and the last contributor (atomic ticket, self-resetting)
-//     applies the epilogue and re-zeroes it -- no latency-serial fix-up on
-//     the tail (summation order across CTAs is not fixed, so shared tiles are
-//     reproducible to f32 rounding, not bitwise);
-//   * warp roles: warp 0 drives the TMA engine (dense operands as 2-D tiled
-//     boxes; gathered neuron rows with sm_100 `tile::gather4`, 4 rows per
-//     instruction, 32 per stage), all landing 128B-swizzled (K-major rows for
-//     UP; for DOWN the gathered rows are K slices stored MN-major, tcgen05
-//     transposes via the instruction descriptor); warp 1 issues tcgen05.mma
-//     from one thread into one of two TMEM accumulators; warps 2-5 drain the
-//     other accumulator (tcgen05.ld 32x32b) and apply bias / ReLU / residual
-//     / bf16-or-f32 store, so the epilogue of one tile overlaps the main loop
-//     of the next.
+//   * persistent thread-block CLUSTERS split K: the C CTAs of a cluster work
+//     on the same 128-row tile concurrently, each over 1/C of the K blocks
+//     (K = the union size for DOWN, read on the device), and reduce their f32
+//     partial tiles through distributed shared memory (DSMEM) with mbarrier
+//     handshakes -- no global partials, no atomics, deterministic rank-order
+//     sums; clusters loop over tiles (the device-resident union size bounds
+//     the tile count: no host sync, CUDA-graph capturable);
+//   * warp roles: warp 0 drives the TMA engine (B operand, and dense A as
+//     2-D tiles / gathered A as sm_100 tile::gather4 when lsu_mode == 0);
+//     warps 6-9 stream the A operand with 16-byte cp.async (LDGSTS) into the
+//     same 128B-swizzled layout (the default for gathered rows: two copy
+//     engines per SM, ~2x the gather4 rate); warp 1 issues tcgen05.mma from
+//     one thread into one of two TMEM accumulators; warps 2-5 drain the other
+//     accumulator (tcgen05.ld 32x32b) through a shared-memory staging tile and
+//     apply bias / ReLU / residual with 16-byte vector stores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,12 +39,12 @@ namespace {
 constexpr int BM = 128;   // UMMA M
 constexpr int BK = 64;    // K elements per stage (one 128-byte swizzle row)
 constexpr int kEpiThreads = 128;
-constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue, warps 6-9 LSU loaders
 constexpr int kMaxNB = 256;
-constexpr int kTicketBytes = 65536;
-constexpr int kMinItersPerCta = 4;
-constexpr int kEpiCols = 64;  // batch rows staged per epilogue pass (32 KB of smem)
-constexpr int kProdWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2;
+constexpr int kEpiCols = 64;   // batch rows staged per epilogue pass (32 KB of smem)
+constexpr int kProdWarp = 0, kMmaWarp = 1, kEpiWarp0 = 2, kLdWarp0 = 6;
+constexpr int kLdThreads = 128;
+constexpr int kMaxCluster = 8;
 
 enum { MODE_UP = 0, MODE_DOWN = 1 };
 
@@ -69,8 +67,6 @@ struct GGParams {
   int64_t out_ld;
   int out_bf16;
   int vec_ok;  // out / residual rows 16-byte aligned: vector epilogue stores
-  int* tickets;
-  float* partials;            // [tiles][NB][BM] f32 accumulators, zero between calls
   unsigned long long* trace;  // debug: per-CTA timestamps (ps_debug_gemm_trace), NULL normally
 };
 
@@ -80,22 +76,65 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// Stream-K partition of T iterations over G CTAs.
-struct Part {
-  int64_t T;
-  int G;
-  PS_DEV int64_t lo(int c) const { return T * c / G; }
-  // CTA whose range contains iteration `it`
-  PS_DEV int owner(int64_t it) const {
-    int c = (int)((it * G) / T);
-    while (c + 1 < G && lo(c + 1) <= it) ++c;
-    while (c > 0 && lo(c) > it) --c;
-    return c;
-  }
-};
+PS_DEV uint32_t sw128(int row, int unit) {  // byte offset of 16B unit `unit` of K-major row `row`
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((unit ^ (row & 7)) << 4));
+}
 
-template <int MODE, bool GATHER>
-__global__ void __launch_bounds__(kThreads, 1)
+PS_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+PS_DEV uint32_t cluster_size() {
+  uint32_t r;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+PS_DEV uint32_t cluster_id() {
+  uint32_t r;
+  asm("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+PS_DEV uint32_t num_clusters() {
+  uint32_t r;
+  asm("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// shared::cta address -> the same offset in CTA `rank` of the cluster
+PS_DEV uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+PS_DEV void remote_arrive(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+PS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+PS_DEV float4 ld_dsmem_v4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// LSU_A: the A operand (weights, gathered or dense) is streamed by 4 loader
+// warps with 16-byte cp.async (LDGSTS) while the TMA engine moves only the B
+// operand.  GATHER: A rows (UP) / K rows (DOWN) are selected by idx.
+template <int MODE, bool GATHER, bool LSU_A>
+__global__ void __launch_bounds__(kThreads, 2)
     gather_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const GGParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -109,12 +148,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* rdy = tempty + 2;    // cluster: every CTA's partial tile staged
+  uint64_t* fre = rdy + 1;       // cluster: every CTA done reading the staged tiles
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fre + 1);
+  float* stg = reinterpret_cast<float*>(smem + S * stage_bytes + 256);  // [kEpiCols][BM] f32
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int cta = blockIdx.x;
-  unsigned long long* tr = p.trace ? p.trace + 16 * (size_t)cta : nullptr;
+  const int C = (int)cluster_size();
+  const int rank = (int)cluster_rank();
+  const int cid = (int)cluster_id(), ncl = (int)num_clusters();
+  unsigned long long* tr = p.trace ? p.trace + 16 * (size_t)blockIdx.x : nullptr;
   if (tr && tid == 0) {
     unsigned smid;
     asm("mov.u32 %0, %smid;" : "=r"(smid));
@@ -122,56 +165,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     tr[7] = smid;
   }
 
-  // ---- device-side work partition (identical in every role)
+  // ---- device-side work partition (identical in every role and CTA of a cluster)
   const int count = p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K);
   const int klimit = (MODE == MODE_UP) ? p.K : count;
   const int kbt = (klimit + BK - 1) / BK;
   const int live_m = (MODE == MODE_UP) ? (count + BM - 1) / BM : (p.M + BM - 1) / BM;
   const int tiles = live_m * p.n_tiles;
-  if (tiles == 0) return;
-  if (kbt == 0) {
-    // DOWN with an empty union: out = bias (+ residual), one tile per CTA
-    if (warp < kEpiWarp0) return;
-    for (int t = cta; t < tiles; t += gridDim.x) {
-      const int mt = t % live_m, nt = t / live_m;
-      const int gm = mt * BM + (tid - kEpiWarp0 * 32);
-      if (gm >= p.M) continue;
-      for (int n = 0; n < NB && nt * NB + n < p.N; ++n) {
-        const int gn = nt * NB + n;
-        float v = p.bias ? p.bias[gm] : 0.f;
-        if (p.residual) v += p.residual[(size_t)gn * p.res_ld + gm];
-        const size_t o = (size_t)gn * p.out_ld + gm;
-        if (p.out_bf16)
-          reinterpret_cast<uint16_t*>(p.out)[o] = f2bf(v);
-        else
-          reinterpret_cast<float*>(p.out)[o] = v;
-      }
-    }
-    return;
-  }
-  Part part;
-  part.T = (int64_t)tiles * kbt;
-  {
-    int64_t g = part.T / kMinItersPerCta;
-    if (g < 1) g = 1;
-    if (g > (int64_t)gridDim.x) g = gridDim.x;
-    part.G = (int)g;
-  }
-  if (cta >= part.G) return;
-  const int64_t it_lo = part.lo(cta), it_hi = part.lo(cta + 1);
-  if (it_lo >= it_hi) return;
+  const int per = (kbt + C - 1) / C;
+  const int kb0 = rank * per;
+  const int nkb = max(0, min(kbt, kb0 + per) - kb0);  // K blocks of this CTA (same for every tile)
+  const int my_tiles = cid < tiles ? (tiles - cid + ncl - 1) / ncl : 0;
+  // every CTA of a cluster sees the same my_tiles, so whole clusters leave together
+  if (my_tiles == 0) return;
 
   const uint32_t tcols = NB <= 16 ? 32 : (NB <= 32 ? 64 : (NB <= 64 ? 128 : (NB <= 128 ? 256 : 512)));
   if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) {
-        mbar_init(&full[s], 1);
+        mbar_init(&full[s], LSU_A ? 1 + kLdThreads : 1);
         mbar_init(&empty[s], 1);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
       }
+      mbar_init(rdy, C);
+      mbar_init(fre, C);
       fence_mbar_init();
     }
     __syncwarp();
@@ -182,14 +201,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  // peers' barriers must be initialised before any remote arrive
+  if (C > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (tr && tid == 0) tr[1] = gtimer();
 
+  auto tile_of = [&](int j) { return cid + j * ncl; };
+
   if (warp == kProdWarp) {
     // ------------------------------------------------------------ TMA producer
-    // 4 gathered ids per lane and stage, loaded one stage ahead (int4) so
-    // the TMA issue never waits on a dependent global load.
     auto load4 = [&](int base, int lim, int first) -> int4 {
       if (base + 4 <= lim) return __ldg(reinterpret_cast<const int4*>(p.idx + base));
       int r[4];
@@ -197,66 +221,125 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 4; ++j) r[j] = base + j < lim ? __ldg(p.idx + base + j) : first;
       return make_int4(r[0], r[1], r[2], r[3]);
     };
-    auto ids_for = [&](int64_t it) -> int4 {
-      if (!GATHER) return make_int4(0, 0, 0, 0);
-      const int t = (int)(it / kbt), kb = (int)(it - (int64_t)t * kbt);
-      if (MODE == MODE_UP) {
-        const int m0 = (t % live_m) * BM;
-        return load4(m0 + lane * 4, count, __ldg(p.idx + m0));  // rows of the tile
-      }
-      return load4(kb * BK + 4 * (lane & 15), count, __ldg(p.idx));  // K rows of the stage
-    };
-    int i = 0;  // global stage counter
-    int4 cur = ids_for(it_lo);
-    for (int64_t it = it_lo; it < it_hi; ++it, ++i) {
-      const int t = (int)(it / kbt), kb = (int)(it - (int64_t)t * kbt);
+    int i = 0;
+    for (int j = 0; j < my_tiles; ++j) {
+      const int t = tile_of(j);
       const int mt = t % live_m, nt = t / live_m;
-      const int m0 = mt * BM, n0 = nt * NB, k0 = kb * BK;
-      const int4 nxt = (it + 1 < it_hi) ? ids_for(it + 1) : cur;
-      const int s = i % S;
-      if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-      uint8_t* sa = smem + s * stage_bytes;
-      uint8_t* sb = sa + a_bytes;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        tma_load_2d(sb, &tmB, k0, n0, &full[s]);  // B: NB batch rows x 64 K
-      }
-      if (GATHER) {
-        if (MODE == MODE_UP) {
-          tma_gather4(sa + lane * 512, &tmA, k0, cur.x, cur.y, cur.z, cur.w, &full[s]);
-        } else {
-          const int c = lane >> 4, j = lane & 15;
-          tma_gather4(sa + c * 8192 + (j >> 1) * 1024 + (j & 1) * 512, &tmA, m0 + 64 * c, cur.x, cur.y, cur.z,
-                      cur.w, &full[s]);
+      const int m0 = mt * BM, n0 = nt * NB;
+      int4 rid = make_int4(0, 0, 0, 0);
+      if (!LSU_A && GATHER && MODE == MODE_UP) rid = load4(m0 + lane * 4, count, __ldg(p.idx + m0));
+      for (int kb = kb0; kb < kb0 + nkb; ++kb, ++i) {
+        const int k0 = kb * BK;
+        int4 kid = make_int4(0, 0, 0, 0);
+        if (!LSU_A && GATHER && MODE == MODE_DOWN) kid = load4(k0 + 4 * (lane & 15), count, __ldg(p.idx));
+        const int s = i % S;
+        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+        uint8_t* sa = smem + s * stage_bytes;
+        uint8_t* sb = sa + a_bytes;
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], LSU_A ? b_bytes : stage_bytes);
+          tma_load_2d(sb, &tmB, k0, n0, &full[s]);  // B: NB batch rows x 64 K
         }
-      } else if (lane == 0) {
+        if (!LSU_A) {
+          if (GATHER) {
+            if (MODE == MODE_UP) {
+              tma_gather4(sa + lane * 512, &tmA, k0, rid.x, rid.y, rid.z, rid.w, &full[s]);
+            } else {
+              const int c = lane >> 4, jj = lane & 15;
+              tma_gather4(sa + c * 8192 + (jj >> 1) * 1024 + (jj & 1) * 512, &tmA, m0 + 64 * c, kid.x, kid.y,
+                          kid.z, kid.w, &full[s]);
+            }
+          } else if (lane == 0) {
+            if (MODE == MODE_UP) {
+              tma_load_2d(sa, &tmA, k0, m0, &full[s]);  // 128 rows x 64 K
+            } else {
+              tma_load_2d(sa, &tmA, m0, k0, &full[s]);  // 64 K rows x 64 MN, two MN chunks
+              tma_load_2d(sa + 8192, &tmA, m0 + 64, k0, &full[s]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= kLdWarp0) {
+    // ------------------------------------------------------------ LSU A loaders (warps 6..9)
+    if (LSU_A) {
+      const int lt = tid - kLdWarp0 * 32;  // 0..127
+      int i = 0;
+      for (int j = 0; j < my_tiles; ++j) {
+        const int t = tile_of(j);
+        const int m0 = (t % live_m) * BM;
+        const uint16_t* src[8];  // UP: this thread's 8 rows of the tile
         if (MODE == MODE_UP) {
-          tma_load_2d(sa, &tmA, k0, m0, &full[s]);  // 128 rows x 64 K
-        } else {
-          tma_load_2d(sa, &tmA, m0, k0, &full[s]);  // 64 K rows x 64 MN, two MN chunks
-          tma_load_2d(sa + 8192, &tmA, m0 + 64, k0, &full[s]);
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int gr = m0 + (lt >> 3) + 16 * r;
+            const int id = gr < count ? (GATHER ? __ldg(p.idx + gr) : gr) : -1;
+            src[r] = id >= 0 ? p.w + (size_t)id * p.w_ld + (lt & 7) * 8 : nullptr;
+          }
+        }
+        int kid[8];  // DOWN: ids of this thread's 8 K rows of the current stage (prefetched)
+        auto down_ids = [&](int kb, int* o) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int kg = kb * BK + (lt >> 4) + 8 * r;
+            o[r] = kg < count ? (GATHER ? __ldg(p.idx + kg) : kg) : -1;
+          }
+        };
+        if (MODE == MODE_DOWN && nkb > 0) down_ids(kb0, kid);
+        for (int kb = kb0; kb < kb0 + nkb; ++kb, ++i) {
+          const int k0 = kb * BK;
+          int kid_next[8];
+          if (MODE == MODE_DOWN && kb + 1 < kb0 + nkb) down_ids(kb + 1, kid_next);
+          const int s = i % S;
+          if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+          uint8_t* sa = smem + s * stage_bytes;
+          if (MODE == MODE_UP) {
+            const int u = lt & 7;
+            const bool kok = k0 + u * 8 < p.K;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const int row = (lt >> 3) + 16 * r;
+              const bool ok = kok && src[r] != nullptr;
+              cp_async16(sa + sw128(row, u), ok ? (const void*)(src[r] + k0) : (const void*)p.w, ok ? 16u : 0u);
+            }
+          } else {
+            // 64 K rows x 128 output features, MN-major SW128 atoms (8 K x 64 MN);
+            // 16 lanes read one 256-byte K row
+            const int mu = lt & 15;
+            const int gm = m0 + mu * 8;
+            const bool mok = gm < p.M;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const int kk = (lt >> 4) + 8 * r;
+              const bool ok = mok && kid[r] >= 0;
+              const void* srcp = ok ? (const void*)(p.w + (size_t)kid[r] * p.w_ld + gm) : (const void*)p.w;
+              const uint32_t off = (uint32_t)((mu >> 3) * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 +
+                                              (((mu & 7) ^ (kk & 7)) << 4));
+              cp_async16(sa + off, srcp, ok ? 16u : 0u);
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) kid[r] = kid_next[r];
+          }
+          cp_async_arrive_noinc(&full[s]);
         }
       }
-      cur = nxt;
-      __syncwarp();
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = make_idesc_bf16(BM, NB, MODE == MODE_DOWN ? 1 : 0, 0);
-      int i = 0, seg = 0;
-      int64_t it = it_lo;
-      while (it < it_hi) {
-        const int t = (int)(it / kbt);
-        const int64_t seg_end = min(it_hi, (int64_t)(t + 1) * kbt);
-        const int a = seg & 1;
-        if (seg >= 2) mbar_wait(&tempty[a], ((seg >> 1) - 1) & 1);
+      int i = 0;
+      for (int j = 0; j < my_tiles; ++j) {
+        const int a = j & 1;
+        if (j >= 2) mbar_wait(&tempty[a], ((j >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t acc = tmem + a * NB;
-        for (int64_t j = it; j < seg_end; ++j, ++i) {
+        for (int kb = 0; kb < nkb; ++kb, ++i) {
           const int s = i % S;
           mbar_wait(&full[s], (i / S) & 1);
           if (tr && i == 0) tr[2] = gtimer();
+          if (LSU_A) fence_proxy_async();  // generic-proxy cp.async writes -> async-proxy MMA reads
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint32_t sb = sa + a_bytes;
@@ -268,47 +351,56 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               ad = make_sdesc_sw128(sa + kk * 2048, 8192, 1024);
             bd = make_sdesc_sw128(sb + kk * 32, 16, 1024);
-            umma_bf16(acc, ad, bd, idesc, (j > it || kk > 0) ? 1u : 0u);
+            umma_bf16(acc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
-        umma_commit(&tfull[a]);
-        it = seg_end;
-        ++seg;
+        if (nkb > 0)
+          umma_commit(&tfull[a]);
+        else
+          mbar_arrive(&tfull[a]);  // this CTA has no K blocks: its partial is zero
       }
       if (tr) tr[3] = gtimer();
     }
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
-    // TMEM -> registers -> smem staging tile S[n][m] (f32) -> 16-byte vector
-    // stores / reductions along m, 4 output columns per operation.
     const int q = warp & 3;               // TMEM lane quadrant of this warp
     const int m = q * 32 + lane;          // tile row (TMEM lane)
     const int et = tid - kEpiWarp0 * 32;  // 0..127
-    float* stg = reinterpret_cast<float*>(smem + S * stage_bytes + 256);  // [kEpiCols][BM]
-    int seg = 0;
-    int64_t it = it_lo;
-    while (it < it_hi) {
-      const int t = (int)(it / kbt);
-      const int64_t t_lo = (int64_t)t * kbt, t_hi = t_lo + kbt;
-      const int64_t seg_end = min(it_hi, t_hi);
-      const int a = seg & 1;
+    // this CTA finishes rows [rank*rows, (rank+1)*rows) of every tile; each
+    // thread always owns the same 4 consecutive output rows (columns of out)
+    const int rows = BM / C;
+    const int vec_per_n = rows / 4;
+    const int my_m = rank * rows + (et % vec_per_n) * 4;
+    int use = 0;  // rdy / fre phase counter
+    const uint32_t stg_s = smem_u32(stg);
+    uint32_t peer_stg[kMaxCluster], peer_rdy[kMaxCluster], peer_fre[kMaxCluster];
+#pragma unroll
+    for (int c = 0; c < kMaxCluster; ++c) {
+      if (c < C) {
+        peer_stg[c] = map_peer(stg_s, c);
+        peer_rdy[c] = map_peer(smem_u32(rdy), c);
+        peer_fre[c] = map_peer(smem_u32(fre), c);
+      }
+    }
+    for (int j = 0; j < my_tiles; ++j) {
+      const int t = tile_of(j);
+      const int a = j & 1;
       const int mt = t % live_m, nt = t / live_m;
       const int m0 = mt * BM, n0 = nt * NB;
       const int nrows = min(NB, p.N - n0);
-      // contributors of tile t: CTAs owning t_lo .. t_hi-1
-      const int c_first = (it == t_lo) ? cta : part.owner(t_lo);
-      const int c_last = (seg_end == t_hi) ? cta : part.owner(t_hi - 1);
-      const bool direct = c_first == c_last;
-      // shared tiles: contributors add partial sums into the tile's f32
-      // accumulator with vector reductions; the last to arrive applies the
-      // epilogue and re-zeroes the accumulator for the next call
-      float* tacc = p.partials + (size_t)t * NB * BM;
-
-      // epilogue for 4 consecutive output columns gm0..gm0+3 of batch row n
-      auto finish4 = [&](int n, int mc, float4 v) {
-        const int gm0 = m0 + mc;
+      float my_bias[4] = {0.f, 0.f, 0.f, 0.f};
+      bool my_live[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int gm = m0 + my_m + u;
+        my_live[u] = (MODE == MODE_UP) ? gm < count : gm < p.M;
+        if (my_live[u] && p.bias)
+          my_bias[u] = __ldg(p.bias + ((MODE == MODE_UP && p.idx) ? __ldg(p.idx + gm) : gm));
+      }
+      auto finish4 = [&](int n, float4 v) {
+        const int gm0 = m0 + my_m;
         const size_t o = (size_t)(n0 + n) * p.out_ld + gm0;
         float vv[4] = {v.x, v.y, v.z, v.w};
         float res[4] = {0.f, 0.f, 0.f, 0.f};
@@ -318,23 +410,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             res[0] = r4.x; res[1] = r4.y; res[2] = r4.z; res[3] = r4.w;
           } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (gm0 + j < p.M) res[j] = p.residual[(size_t)(n0 + n) * p.res_ld + gm0 + j];
+            for (int u = 0; u < 4; ++u)
+              if (gm0 + u < p.M) res[u] = p.residual[(size_t)(n0 + n) * p.res_ld + gm0 + u];
           }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int gm = gm0 + j;
-          const bool live = (MODE == MODE_UP) ? gm < count : gm < p.M;
+        for (int u = 0; u < 4; ++u) {
           float x = 0.f;
-          if (live) {
-            float bias = 0.f;
-            if (p.bias) bias = __ldg(p.bias + ((MODE == MODE_UP && p.idx) ? __ldg(p.idx + gm) : gm));
-            x = vv[j] + bias;
+          if (my_live[u]) {
+            x = vv[u] + my_bias[u];
             if (MODE == MODE_UP && p.act == PS_ACT_RELU) x = fmaxf(x, 0.f);
-            x += res[j];
+            x += res[u];
           }
-          vv[j] = x;
+          vv[u] = x;
         }
         if (p.vec_ok && gm0 + 4 <= p.M) {
           if (p.out_bf16) {
@@ -347,27 +435,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (gm0 + j >= p.M) break;
+          for (int u = 0; u < 4; ++u) {
+            if (gm0 + u >= p.M) break;
             if (p.out_bf16)
-              reinterpret_cast<uint16_t*>(p.out)[o + j] = f2bf(vv[j]);
+              reinterpret_cast<uint16_t*>(p.out)[o + u] = f2bf(vv[u]);
             else
-              reinterpret_cast<float*>(p.out)[o + j] = vv[j];
+              reinterpret_cast<float*>(p.out)[o + u] = vv[u];
           }
         }
       };
 
-      mbar_wait(&tfull[a], (seg >> 1) & 1);
-      if (tr && et == 0 && seg == 0) tr[8] = gtimer();
+      mbar_wait(&tfull[a], (j >> 1) & 1);
+      if (tr && et == 0 && j == 0) tr[8] = gtimer();
       tc_fence_after();
       for (int cb = 0; cb < NB; cb += kEpiCols) {
         const int ncb = min(kEpiCols, NB - cb);
+        // 1) this CTA's partial (or zero) -> staging tile stg[n][m]
         for (int c0 = 0; c0 < ncb; c0 += 16) {
           uint32_t r[16];
-          tmem_ld16(tmem + a * NB + ((uint32_t)(q * 32) << 16) + cb + c0, r);
-          tmem_ld_wait();
+          if (nkb > 0) {
+            tmem_ld16(tmem + a * NB + ((uint32_t)(q * 32) << 16) + cb + c0, r);
+            tmem_ld_wait();
+          } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) stg[(c0 + j) * BM + m] = __uint_as_float(r[j]);
+            for (int u = 0; u < 16; ++u) r[u] = 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) stg[(c0 + u) * BM + m] = __uint_as_float(r[u]);
         }
         if (cb + kEpiCols >= NB) {
           tc_fence_before();
@@ -376,62 +470,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
         const int rows_here = min(ncb, nrows - cb);
-        for (int v = et; v < rows_here * (BM / 4); v += kEpiThreads) {
-          const int n = v / (BM / 4), mc = (v % (BM / 4)) * 4;
-          const float4 val = *reinterpret_cast<const float4*>(stg + n * BM + mc);
-          if (direct)
-            finish4(cb + n, mc, val);
-          else
-            red_add_v4(tacc + (size_t)(cb + n) * BM + mc, val);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
-      }
-      if (tr && et == 0 && seg == 0) tr[9] = gtimer();
-
-      if (!direct) {
-        __threadfence();
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
-        if (et == 0) {
-          const int prev = atomicAdd(p.tickets + t, 1);
-          *flag = prev == (c_last - c_first);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
-        const bool last = *flag;
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
-        if (last) {
-          __threadfence();
-          const int nv = nrows * (BM / 4);
-          for (int v0 = et; v0 < nv; v0 += 4 * kEpiThreads) {
-            float4 val[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int v = v0 + u * kEpiThreads;
-              val[u] = v < nv ? __ldcg(reinterpret_cast<const float4*>(tacc) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int v = v0 + u * kEpiThreads;
-              if (v < nv) {
-                finish4(v / (BM / 4), (v % (BM / 4)) * 4, val[u]);
-                __stcg(reinterpret_cast<float4*>(tacc) + v, make_float4(0.f, 0.f, 0.f, 0.f));
-              }
-            }
+        if (C == 1) {
+          for (int v = et; v < rows_here * vec_per_n; v += kEpiThreads) {
+            const int n = v / vec_per_n;
+            finish4(cb + n, *reinterpret_cast<const float4*>(stg + n * BM + my_m));
           }
-          if (et == 0) p.tickets[t] = 0;
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+        } else {
+          // 2) every CTA staged: reduce my rows over the C partials in rank order
+          if (et == 0)
+            for (int c = 0; c < C; ++c) remote_arrive(peer_rdy[c]);
+          mbar_wait_cluster(rdy, use & 1);
+          for (int v = et; v < rows_here * vec_per_n; v += kEpiThreads) {
+            const int n = v / vec_per_n;
+            const uint32_t off = (uint32_t)((n * BM + my_m) * 4);
+            float4 acc[kMaxCluster];
+#pragma unroll
+            for (int c = 0; c < kMaxCluster; ++c)
+              if (c < C) acc[c] = ld_dsmem_v4(peer_stg[c] + off);
+            float4 sum = acc[0];
+#pragma unroll
+            for (int c = 1; c < kMaxCluster; ++c)
+              if (c < C) {
+                sum.x += acc[c].x; sum.y += acc[c].y; sum.z += acc[c].z; sum.w += acc[c].w;
+              }
+            finish4(cb + n, sum);
+          }
+          // 3) done reading the peers' staging tiles
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+          if (et == 0)
+            for (int c = 0; c < C; ++c) remote_arrive(peer_fre[c]);
+          mbar_wait_cluster(fre, use & 1);
+          ++use;
         }
       }
-      if (tr && et == 0 && seg == 0) tr[10] = gtimer();
-      it = seg_end;
-      ++seg;
+      if (tr && et == 0 && j == 0) tr[9] = gtimer();
     }
     if (tr && et == 0) tr[4] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
-  if (tr && tid == 0) {
-    tr[5] = gtimer();
-    tr[6] = it_hi - it_lo;
-  }
+  if (tr && tid == 0) tr[5] = gtimer();
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, tcols);
@@ -445,6 +524,7 @@ int pick_nb(int N) {
 
 unsigned long long* g_trace = nullptr;
 int g_stages_override = 0, g_target_override = 0;
+int g_lsu_mode = 1;  // 0: TMA for A, 1: LSU for gathered A, 2: LSU for all A
 
 int ctas_per_sm(int NB) { return NB <= 128 ? 2 : 1; }
 
@@ -462,7 +542,15 @@ size_t smem_bytes(int NB, int stages) {
   return 1024 + (size_t)stages * (BM * BK * 2 + NB * BK * 2) + 256 + (size_t)kEpiCols * BM * 4;
 }
 
-int grid_ctas(int NB) { return g_target_override > 0 ? g_target_override : ps_num_sms() * ctas_per_sm(NB); }
+int cta_slots(int NB) { return g_target_override > 0 ? g_target_override : ps_num_sms() * ctas_per_sm(NB); }
+
+// cluster size: enough CTAs per tile to fill every CTA slot, >= 2 K blocks each
+int pick_cluster(int NB, int tiles_est, int kbt) {
+  const int slots = cta_slots(NB);
+  int c = 1;
+  while (c < kMaxCluster && tiles_est * c * 2 <= slots && (kbt / (c * 2)) >= 2) c *= 2;
+  return c;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -490,23 +578,39 @@ int make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uin
   return r == CUDA_SUCCESS ? PS_OK : PS_ERR_VALUE;
 }
 
-template <int MODE, bool GATHER>
-int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, GGParams& prm, cudaStream_t st) {
+template <int MODE, bool GATHER, bool LSU_A>
+int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GGParams& prm, int cluster, cudaStream_t st) {
   const size_t smem = smem_bytes(prm.NB, prm.stages);
-  auto kern = gather_gemm_kernel<MODE, GATHER>;
+  auto kern = gather_gemm_kernel<MODE, GATHER, LSU_A>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return PS_ERR_CUDA;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return PS_ERR_CUDA;
     configured = true;
   }
-  kern<<<grid_ctas(prm.NB), kThreads, smem, st>>>(ta, tb, prm);
+  const int grid = (cta_slots(prm.NB) / cluster) * cluster;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, prm) != cudaSuccess) return PS_ERR_CUDA;
   return launch_status();
 }
 
 // w_rows: (w_rows_n, w_cols) row-major; B operand x: (N, kx) with row stride x_ld
 template <int MODE>
-int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, cudaStream_t st) {
+int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, int tiles_est, int kbt_est,
+           cudaStream_t st) {
   CUtensorMap ta, tb;
   int rc = make_map(&tb, prm.x, (uint64_t)kx, (uint64_t)prm.N, (uint64_t)prm.x_ld, BK, prm.NB);
   if (rc != PS_OK) return rc;
@@ -516,7 +620,13 @@ int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, cudaStre
   else
     rc = make_map(&ta, prm.w, (uint64_t)w_cols, (uint64_t)w_rows_n, (uint64_t)prm.w_ld, 64, gather ? 1 : BK);
   if (rc != PS_OK) return rc;
-  return gather ? launch_t<MODE, true>(ta, tb, prm, st) : launch_t<MODE, false>(ta, tb, prm, st);
+  const int cluster = pick_cluster(prm.NB, tiles_est * prm.n_tiles, kbt_est);
+  const bool lsu = g_lsu_mode == 2 || (g_lsu_mode == 1 && gather);
+  if (gather)
+    return lsu ? launch_t<MODE, true, true>(ta, tb, prm, cluster, st)
+               : launch_t<MODE, true, false>(ta, tb, prm, cluster, st);
+  return lsu ? launch_t<MODE, false, true>(ta, tb, prm, cluster, st)
+             : launch_t<MODE, false, false>(ta, tb, prm, cluster, st);
 }
 
 }  // namespace
@@ -524,26 +634,24 @@ int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, cudaStre
 
 using namespace ps;
 
+// The cluster kernel reduces split-K partials on chip: only a token
+// workspace is needed (kept in the ABI for callers that size one).
 extern "C" size_t ps_gather_gemm_workspace_bytes(int N, int M, int K, int splits) {
-  (void)K;
-  (void)splits;
-  if (N < 1 || M < 1) return 0;
-  const int NB = pick_nb(N);
-  const size_t tiles = (size_t)((M + BM - 1) / BM) * ((N + NB - 1) / NB);
-  return kTicketBytes + tiles * NB * BM * 4;
+  (void)N; (void)M; (void)K; (void)splits;
+  return 256;
 }
 
-// Kept for ABI compatibility: the persistent stream-K kernel partitions the
-// work on the device, so the split count is always chosen there.
+// `splits` argument of ps_gather_gemm(_t) = expected live union size (rows
+// for UP, K for DOWN) used to size the K-split clusters; 0 = the maximum.
 extern "C" int ps_gather_gemm_auto_splits(int N, int M, int K) {
   (void)N; (void)M; (void)K;
-  return 1;
+  return 0;
 }
 
 static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, const int32_t* count_dev,
                      const void* x, int64_t x_ld, const float* bias, int N, int M, int K, void* out, int64_t out_ld,
-                     int out_dtype, void* ws, size_t ws_bytes) {
-  if (N < 1 || M < 1 || K < 1 || !w_rows || !x || !out || !ws) return PS_ERR_VALUE;
+                     int out_dtype) {
+  if (N < 1 || M < 1 || K < 1 || !w_rows || !x || !out) return PS_ERR_VALUE;
   if (((uintptr_t)w_rows % 16) || ((uintptr_t)x % 16) || (x_ld % 8)) return PS_ERR_VALUE;
   prm.w = static_cast<const uint16_t*>(w_rows);
   prm.idx = idx;
@@ -565,9 +673,6 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
   prm.out_ld = out_ld;
   prm.out_bf16 = out_dtype == PS_DTYPE_BF16;
   prm.vec_ok = (out_ld % 4 == 0) && ((uintptr_t)out % 16 == 0);
-  if (ws_bytes < ps_gather_gemm_workspace_bytes(N, M, K, 1)) return PS_ERR_WORKSPACE;
-  prm.tickets = static_cast<int*>(ws);
-  prm.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
   return PS_OK;
 }
 
@@ -575,44 +680,52 @@ extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* i
                               const void* x, int64_t x_ld, const float* bias, const float* residual,
                               int64_t residual_ld, int N, int M, int K, int act, int splits, void* out, int64_t out_ld,
                               int out_dtype, void* ws, size_t ws_bytes, void* stream) {
-  (void)splits;
+  (void)ws; (void)ws_bytes;
   if (K % 8 || x_ld < K || out_ld < M) return PS_ERR_VALUE;
   GGParams prm;
-  int st = gg_common(prm, w_rows, idx, count_dev, x, x_ld, bias, N, M, K, out, out_ld, out_dtype, ws, ws_bytes);
+  int st = gg_common(prm, w_rows, idx, count_dev, x, x_ld, bias, N, M, K, out, out_ld, out_dtype);
   if (st != PS_OK) return st;
   prm.w_ld = K;
   prm.act = act;
   prm.residual = residual;
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;
-  if ((size_t)((M + BM - 1) / BM) * prm.n_tiles * 4 > kTicketBytes) return PS_ERR_UNSUPPORTED;
   if (w_height < (idx ? 1 : M)) return PS_ERR_VALUE;
-  return launch<MODE_UP>(prm, w_height, K, K, static_cast<cudaStream_t>(stream));
+  const int rows_est = splits > 0 ? (splits < M ? splits : M) : M;
+  return launch<MODE_UP>(prm, w_height, K, K, (rows_est + BM - 1) / BM, (K + BK - 1) / BK,
+                         static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                                 const void* h, int64_t h_ld, const float* bias, const float* residual,
                                 int64_t residual_ld, int N, int M, int K_max, int splits, void* out, int64_t out_ld,
                                 int out_dtype, void* ws, size_t ws_bytes, void* stream) {
-  (void)splits;
+  (void)ws; (void)ws_bytes;
   if (M % 8 || h_ld < K_max || out_ld < M) return PS_ERR_VALUE;
   GGParams prm;
-  int st = gg_common(prm, w_rows, idx, count_dev, h, h_ld, bias, N, M, K_max, out, out_ld, out_dtype, ws, ws_bytes);
+  int st = gg_common(prm, w_rows, idx, count_dev, h, h_ld, bias, N, M, K_max, out, out_ld, out_dtype);
   if (st != PS_OK) return st;
   prm.w_ld = M;
   prm.residual = residual;
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;
-  if ((size_t)((M + BM - 1) / BM) * prm.n_tiles * 4 > kTicketBytes) return PS_ERR_UNSUPPORTED;
   if (w_height < (idx ? 1 : K_max)) return PS_ERR_VALUE;
-  return launch<MODE_DOWN>(prm, w_height, M, K_max, static_cast<cudaStream_t>(stream));
+  // the K extent (union size) is read on the device; `splits` > 0 is its expected value
+  const int k_est = splits > 0 ? (splits < K_max ? splits : K_max) : K_max;
+  return launch<MODE_DOWN>(prm, w_height, M, K_max, (M + BM - 1) / BM, (k_est + BK - 1) / BK,
+                           static_cast<cudaStream_t>(stream));
 }
 
 // Debug hooks (tools/kbench.py): trace buffer of 16 u64 per CTA (start, setup
-// done, first stage landed, last MMA issued, epilogue done, end, iterations,
-// smid, first accumulator ready, first drained, first segment finished), and overrides of the pipeline depth / persistent grid (0 = default).
+// done, first stage landed, last MMA issued, epilogue done, end, -, smid,
+// first accumulator ready, first tile finished), and overrides of the
+// pipeline depth / CTA slots (0 = default).
 extern "C" void ps_debug_gemm_trace(void* buf, int stages, int target_ctas) {
   g_trace = static_cast<unsigned long long*>(buf);
   g_stages_override = stages;
   g_target_override = target_ctas;
 }
+
+// A-operand copy engine: 0 = TMA only, 1 = LSU for gathered rows (default),
+// 2 = LSU for every A operand.
+extern "C" void ps_debug_gemm_lsu_mode(int mode) { g_lsu_mode = mode; }

@@ -325,7 +325,7 @@ class DecodeEngine:
                         self.union_idx[: int(self.union_count.item())].clone())
                 if self.tp is None:
                     mlp_into(lw.mlp, self.h, self.union_idx, self.union_count, self.hidden, self.x,
-                             residual=self.x)
+                             residual=self.x, expected=self.k_mlp[ell])
                     n += 2
                 else:
                     n += self.tp.mlp(self, lw, self.union_idx, self.union_count)

@@ -344,7 +344,7 @@ def _mlp_packed(x, w1, b1, w2, b2, w3=None) -> PackedMLP:
 
 
 def mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor, out: torch.Tensor,
-             residual=None, splits_up=0, splits_down=0) -> None:
+             residual=None, splits_up=0, splits_down=0, expected=0) -> None:
     """relu(x W1[:, S] + b1[S]) W2[:, S]^T + b2 (+ residual) into ``out``.
 
     ``idx``/``count`` = None runs the dense MLP through the same kernels.
@@ -352,11 +352,11 @@ def mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor,
     """
     B, d = x2d.shape
     gather_gemm_into(pk.w1t, idx, count, x2d, x2d.stride(0), pk.b1, B, pk.D if idx is None else pk.D_pad,
-                     d, _lib.PS_ACT_RELU, hidden, hidden.stride(0), splits=splits_up, tag="gg_up")
+                     d, _lib.PS_ACT_RELU, hidden, hidden.stride(0), splits=splits_up or expected, tag="gg_up")
     gather_gemm_t_into(pk.w2t, idx, count, hidden, hidden.stride(0), pk.b2, B, d,
                        pk.D if idx is None else pk.D_pad, out, out.stride(0),
                        residual=residual, res_ld=0 if residual is None else residual.stride(0),
-                       splits=splits_down, tag="gg_down")
+                       splits=splits_down or expected, tag="gg_down")
 
 
 def sparse_mlp_forward(x, w1, b1=None, w2=None, b2=None, active=None) -> torch.Tensor:

@@ -1,0 +1,94 @@
+"""Tensor-parallel decode step on the device path: 2 ranks sharing one GPU
+(gloo carries the CUDA partial sums; NCCL needs distinct GPUs), each running
+its shard engine (group_base-offset SHA, [lo, hi) union compaction, shard
+GEMMs).  Must match the TP=1 engine on the same model and inputs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _build(kv_heads, mode, tp=None, plan=None):
+    from oracle import polar_oracle as po
+    import paper_2505_14884_b200 as pb
+    from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy
+    from paper_2505_14884_b200.model import DeviceModel, TransformerConfig
+    from paper_2505_14884_b200.parallel import shard_model
+
+    cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 288, "relu")
+    host = po.random_model(2, 256, 1024, 8, kv_heads, 512, 288, seed=21)
+    model = DeviceModel.from_host(cfg, host)
+    if plan is not None:
+        model = shard_model(model, plan)
+    polar = mode == "polar"
+    policy = SparsityPolicy(mode=mode, mlp_k_table={0: 128, 1: 128} if polar else None,
+                            head_density=0.5 if polar else 1.0)
+    hr = [pb.HeadRouter(256, kv_heads, seed=40 + e) for e in range(2)]
+    mr = [pb.MlpRouter(256, 1024, seed=30 + e) for e in range(2)]
+    eng = DecodeEngine(model, 8, 288, policy, head_routers=hr, mlp_routers=mr, tp=tp)
+    rng = np.random.default_rng(22)
+    g0 = 0 if plan is None else plan.group_base
+    nl = kv_heads if plan is None else plan.kv_heads_local
+    for c in eng.caches:
+        k = rng.standard_normal((8, kv_heads, 256, 32), dtype=np.float32)
+        v = rng.standard_normal((8, kv_heads, 256, 32), dtype=np.float32)
+        c.keys[:, :, :256] = torch.from_numpy(k[:, g0:g0 + nl]).cuda().bfloat16()
+        c.values[:, :, :256] = torch.from_numpy(v[:, g0:g0 + nl]).cuda().bfloat16()
+        c.set_lengths([256] * 8)
+    tokens = rng.integers(0, 512, 8, dtype=np.int64)
+    return eng, tokens
+
+
+def _rank(rank, world, port, kv_heads, mode, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2505_14884_b200.model import TransformerConfig
+        from paper_2505_14884_b200.parallel import TPPlan, TensorParallel
+
+        cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 288, "relu")
+        plan = TPPlan.make(cfg, world, rank)
+        eng, tokens = _build(kv_heads, mode, tp=TensorParallel(plan), plan=plan)
+        logits = eng.step(tokens).cpu().numpy()
+        if rank == 0:
+            ref_eng, _ = _build(kv_heads, mode)
+            ref = ref_eng.step(tokens).cpu().numpy()
+            q.put((float(np.abs(logits - ref).max()), float(np.abs(ref).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kv_heads,mode", [(8, "polar"), (2, "polar"), (8, "dense")])
+def test_tp2_device_matches_tp1(kv_heads, mode):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_rank, args=(r, 2, port, kv_heads, mode, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    err, scale = q.get(timeout=10)
+    assert err <= 2e-2 * max(1.0, scale), err

@@ -153,7 +153,7 @@ def trace_main():
     dev = torch.device("cuda")
     B, d, D = a.batch, a.d, a.D
     L = _lib.load()
-    buf = torch.zeros(8 * 200000, dtype=torch.int64, device=dev)
+    buf = torch.zeros(16 * 4000, dtype=torch.int64, device=dev)
     w = [(torch.randn(D, d, device=dev) * 0.02).bfloat16() for _ in range(4)]
     x = torch.randn(B, d, device=dev).bfloat16()
     k = int(a.union * D)
