@@ -79,6 +79,20 @@ class KVCache:
         self.host_lengths = np.zeros(batch, dtype=np.int64)
         self._err = torch.zeros(1, dtype=torch.int32, device=device)
 
+    @classmethod
+    def from_reference(cls, cache, device="cuda") -> "KVCache":
+        """Device copy of a reference ``KVCache`` (tensors.py:116-148 fields
+        ``keys``/``values`` f32 (B, H_kv, cap, d_h) and ``lengths``), rounded
+        to bf16.  Used by the parity adapter only (a full H2D copy)."""
+        keys = np.asarray(cache.keys)
+        b, h, cap, d_h = keys.shape
+        out = cls(b, h, cap, d_h, device=device)
+        out.keys.copy_(torch.from_numpy(np.ascontiguousarray(keys, dtype=np.float32)))
+        out.values.copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(cache.values), dtype=np.float32)))
+        out.host_lengths[:] = np.asarray(cache.lengths, dtype=np.int64)
+        out._sync_lengths()
+        return out
+
     @property
     def batch(self) -> int:
         return self.keys.shape[0]
