@@ -113,13 +113,18 @@ int ps_topk_rows(const float* logits, int rows, int cols, int64_t ld, int k,
 int ps_threshold_rows(const float* logits, int rows, int cols, int64_t ld, float thr,
                       uint32_t* bitmap, void* stream);
 /* Fused per-row selection + union + compaction (one launch per layer): top-k
- * (k > 0) or threshold (k <= 0: logit > thr) per row ORed into `bitmap`, then
- * the last CTA compacts bits [lo, hi) into union_out / count_out exactly as
- * ps_bitmap_compact does and clears the bitmap.  `ticket`: one int32,
- * zero-filled before first use (self-resetting). */
+ * (k > 0) or threshold (k <= 0: logit > thr) per row; each row's selection
+ * words are stored into the workspace, the last CTA of every 16-row group
+ * ORs the group, and the last group compacts bits [lo, hi) into union_out /
+ * count_out exactly as ps_bitmap_compact does.  No contended atomics.
+ * ws >= ps_select_union_workspace_bytes(rows, cols), zero-filled before its
+ * first use (its tickets self-reset; the bitmaps are fully rewritten). */
+size_t ps_select_union_workspace_bytes(int rows, int cols);
 int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr,
-                    uint32_t* bitmap, int* ticket, int lo, int hi, int pad,
+                    void* ws, size_t ws_bytes, int lo, int hi, int pad,
                     int32_t* union_out, int32_t* count_out, void* stream);
+/* debug: per-CTA phase timestamps of the top-k kernel (16 x u64 per CTA), NULL = off */
+void ps_debug_topk_trace(void* buf);
 int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width,
                   uint32_t* bitmap, void* stream);
 int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, int pad,
@@ -193,6 +198,12 @@ int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t* idx, const
  * ==================================================================== */
 int ps_layernorm(const float* x, int64_t x_ld, const float* gamma, const float* beta,
                  int B, int d, void* y, int64_t y_ld, void* stream);
+/* ps_add_layernorm: x += add (f32 (d), may be NULL; written back -- the
+ *   bias of the projection whose GEMM just accumulated into x, e.g. b_o of
+ *   engine.py:368 or b2 of kernels.py:372), then y = layernorm(x) as above.
+ *   d % 4 == 0, 16-byte aligned rows. */
+int ps_add_layernorm(float* x, int64_t x_ld, const float* add, const float* gamma, const float* beta,
+                     int B, int d, void* y, int64_t y_ld, void* stream);
 /* ps_swiglu: the gated activation of swiglu_mlp_forward (kernels.py:335-350):
  *   h[b, j] = silu(gu[b, j]) * gu[b, D + j]   (bf16 in/out, f32 math)     */
 int ps_swiglu(const void* gu, int64_t gu_ld, int B, int D, void* h, int64_t h_ld, void* stream);

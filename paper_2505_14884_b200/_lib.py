@@ -38,12 +38,14 @@ SIGNATURES = {
     "ps_kv_append": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _i, _i, _i, _i, _vp, _vp]),
     "ps_topk_rows": (_i, [_vp, _i, _i, _i64, _i, _vp, _vp, _vp]),
     "ps_threshold_rows": (_i, [_vp, _i, _i, _i64, _f, _vp, _vp]),
-    "ps_select_union": (_i, [_vp, _i, _i, _i64, _i, _f, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "ps_select_union_workspace_bytes": (_sz, [_i, _i]),
+    "ps_select_union": (_i, [_vp, _i, _i, _i64, _i, _f, _vp, _sz, _i, _i, _i, _vp, _vp, _vp]),
     "ps_union_rows": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ps_bitmap_compact": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_head_router_topk": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_debug_gemm_trace": (None, [_vp, _i, _i]),
     "ps_debug_gemm_lsu_mode": (None, [_i]),
+    "ps_debug_topk_trace": (None, [_vp]),
     "ps_gather_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "ps_gather_gemm_auto_splits": (_i, [_i, _i, _i]),
     "ps_gather_gemm": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i,
@@ -51,6 +53,7 @@ SIGNATURES = {
     "ps_gather_gemm_t": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i,
                               _vp, _i64, _i, _vp, _sz, _vp]),
     "ps_layernorm": (_i, [_vp, _i64, _vp, _vp, _i, _i, _vp, _i64, _vp]),
+    "ps_add_layernorm": (_i, [_vp, _i64, _vp, _vp, _vp, _i, _i, _vp, _i64, _vp]),
     "ps_embed": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp]),
     "ps_swiglu": (_i, [_vp, _i64, _i, _i, _vp, _i64, _vp]),
 }

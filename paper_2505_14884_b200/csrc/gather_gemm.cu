@@ -80,16 +80,6 @@ PS_DEV uint32_t sw128(int row, int unit) {  // byte offset of 16B unit `unit` of
   return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((unit ^ (row & 7)) << 4));
 }
 
-PS_DEV uint32_t cluster_rank() {
-  uint32_t r;
-  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-PS_DEV uint32_t cluster_size() {
-  uint32_t r;
-  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
 PS_DEV uint32_t cluster_id() {
   uint32_t r;
   asm("mov.u32 %0, %%clusterid.x;" : "=r"(r));
@@ -98,12 +88,6 @@ PS_DEV uint32_t cluster_id() {
 PS_DEV uint32_t num_clusters() {
   uint32_t r;
   asm("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-// shared::cta address -> the same offset in CTA `rank` of the cluster
-PS_DEV uint32_t map_peer(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
 PS_DEV void remote_arrive(uint32_t bar_cluster_addr) {

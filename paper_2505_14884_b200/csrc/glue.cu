@@ -8,10 +8,17 @@ namespace ps {
 namespace {
 
 // one CTA per sequence: copy H_kv*d_h new keys/values to row lengths[b],
-// then bump lengths[b].  A full sequence is left untouched (err_flag = 1).
-__global__ void kv_append_kernel(uint16_t* __restrict__ kc, uint16_t* __restrict__ vc, int32_t* __restrict__ lengths,
-                                 const uint16_t* __restrict__ kn, const uint16_t* __restrict__ vn, int64_t src_ld,
-                                 int H_kv, int cap, int d_h, int32_t* err_flag) {
+// then bump lengths[b].  Every thread issues all of its 16-byte loads before
+// its stores (one memory latency per CTA).  A full sequence is left
+// untouched (err_flag = 1).
+constexpr int kKvThreads = 512;
+constexpr int kKvVec = 4;  // 16-byte vectors per thread per tensor (H_kv*d_h <= 16384)
+
+__global__ void __launch_bounds__(kKvThreads) kv_append_kernel(uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
+                                                               int32_t* __restrict__ lengths,
+                                                               const uint16_t* __restrict__ kn,
+                                                               const uint16_t* __restrict__ vn, int64_t src_ld,
+                                                               int H_kv, int cap, int d_h, int32_t* err_flag) {
   const int b = blockIdx.x;
   const int pos = lengths[b];
   if (pos >= cap) {
@@ -20,27 +27,64 @@ __global__ void kv_append_kernel(uint16_t* __restrict__ kc, uint16_t* __restrict
   }
   const int vec_per_head = d_h / 8;
   const int total = H_kv * vec_per_head;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int h = e / vec_per_head, c = e - h * vec_per_head;
-    const size_t dst = (((size_t)b * H_kv + h) * cap + pos) * d_h + c * 8;
-    const size_t src = (size_t)b * src_ld + (size_t)h * d_h + c * 8;
-    *reinterpret_cast<uint4*>(kc + dst) = *reinterpret_cast<const uint4*>(kn + src);
-    *reinterpret_cast<uint4*>(vc + dst) = *reinterpret_cast<const uint4*>(vn + src);
+  for (int e0 = 0; e0 < total; e0 += kKvThreads * kKvVec) {
+    uint4 kr[kKvVec], vr[kKvVec];
+#pragma unroll
+    for (int j = 0; j < kKvVec; ++j) {
+      const int e = e0 + j * kKvThreads + threadIdx.x;
+      if (e < total) {
+        const int h = e / vec_per_head, c = e - h * vec_per_head;
+        const size_t src = (size_t)b * src_ld + (size_t)h * d_h + c * 8;
+        kr[j] = __ldg(reinterpret_cast<const uint4*>(kn + src));
+        vr[j] = __ldg(reinterpret_cast<const uint4*>(vn + src));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kKvVec; ++j) {
+      const int e = e0 + j * kKvThreads + threadIdx.x;
+      if (e < total) {
+        const int h = e / vec_per_head, c = e - h * vec_per_head;
+        const size_t dst = (((size_t)b * H_kv + h) * cap + pos) * d_h + c * 8;
+        *reinterpret_cast<uint4*>(kc + dst) = kr[j];
+        *reinterpret_cast<uint4*>(vc + dst) = vr[j];
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) lengths[b] = pos + 1;
 }
 
+// LayerNorm of one f32 row per CTA held in registers (float4 per slot):
+// optional pending-bias add (x += add, written back -- the bias of the
+// projection whose GEMM wrote x), two-pass mean / variance from registers,
+// bf16 output with 8-byte stores.
 constexpr int kLnThreads = 256;
+constexpr int kLnSlots = 16;  // float4 per thread: d <= 16384
 
-__global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const float* __restrict__ x, int64_t x_ld,
+template <bool ADD>
+__global__ void __launch_bounds__(kLnThreads) layernorm_kernel(float* __restrict__ x, int64_t x_ld,
+                                                               const float* __restrict__ add,
                                                                const float* __restrict__ g,
                                                                const float* __restrict__ bta, int d,
                                                                uint16_t* __restrict__ y, int64_t y_ld) {
   __shared__ float red[2][kLnThreads / 32];
-  const float* xr = x + (size_t)blockIdx.x * x_ld;
+  float* xr = x + (size_t)blockIdx.x * x_ld;
+  const int n4 = d >> 2;
+  float4 v[kLnSlots];
   float s = 0.f;
-  for (int i = threadIdx.x; i < d; i += kLnThreads) s += xr[i];
+#pragma unroll
+  for (int j = 0; j < kLnSlots; ++j) {
+    const int i = j * kLnThreads + threadIdx.x;
+    if (i < n4) {
+      v[j] = *reinterpret_cast<const float4*>(xr + 4 * i);
+      if (ADD) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(add) + i);
+        v[j].x += a.x; v[j].y += a.y; v[j].z += a.z; v[j].w += a.w;
+        *reinterpret_cast<float4*>(xr + 4 * i) = v[j];
+      }
+      s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    }
+  }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = s;
   __syncthreads();
@@ -48,13 +92,17 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const float* __re
 #pragma unroll
   for (int w = 0; w < kLnThreads / 32; ++w) mean += red[0][w];
   mean /= d;
-  float v = 0.f;
-  for (int i = threadIdx.x; i < d; i += kLnThreads) {
-    const float t = xr[i] - mean;
-    v += t * t;
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < kLnSlots; ++j) {
+    const int i = j * kLnThreads + threadIdx.x;
+    if (i < n4) {
+      const float a = v[j].x - mean, b2 = v[j].y - mean, c = v[j].z - mean, e = v[j].w - mean;
+      q += (a * a + b2 * b2) + (c * c + e * e);
+    }
   }
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) red[1][threadIdx.x >> 5] = v;
+  q = warp_sum(q);
+  if ((threadIdx.x & 31) == 0) red[1][threadIdx.x >> 5] = q;
   __syncthreads();
   float var = 0.f;
 #pragma unroll
@@ -62,7 +110,18 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const float* __re
   var /= d;
   const float rstd = rsqrtf(var + 1e-5f);
   uint16_t* yr = y + (size_t)blockIdx.x * y_ld;
-  for (int i = threadIdx.x; i < d; i += kLnThreads) yr[i] = f2bf((xr[i] - mean) * rstd * g[i] + bta[i]);
+#pragma unroll
+  for (int j = 0; j < kLnSlots; ++j) {
+    const int i = j * kLnThreads + threadIdx.x;
+    if (i < n4) {
+      const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + i);
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(bta) + i);
+      uint2 o;
+      o.x = pack_bf16x2((v[j].x - mean) * rstd * gg.x + bb.x, (v[j].y - mean) * rstd * gg.y + bb.y);
+      o.y = pack_bf16x2((v[j].z - mean) * rstd * gg.z + bb.z, (v[j].w - mean) * rstd * gg.w + bb.w);
+      *reinterpret_cast<uint2*>(yr + 4 * i) = o;
+    }
+  }
 }
 
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ len,
@@ -127,18 +186,39 @@ extern "C" int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths, cons
   if (B < 1 || H_kv < 1 || cap < 1 || d_h < 8 || d_h % 8 || src_ld < (int64_t)H_kv * d_h || src_ld % 8)
     return PS_ERR_VALUE;
   if (!k_cache || !v_cache || !lengths || !k_new || !v_new) return PS_ERR_VALUE;
-  kv_append_kernel<<<B, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+  if (((uintptr_t)k_new % 16) || ((uintptr_t)v_new % 16) || ((uintptr_t)k_cache % 16) || ((uintptr_t)v_cache % 16))
+    return PS_ERR_VALUE;
+  kv_append_kernel<<<B, kKvThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths, static_cast<const uint16_t*>(k_new),
       static_cast<const uint16_t*>(v_new), src_ld, H_kv, cap, d_h, err_flag);
   return launch_status();
 }
 
+static int ln_launch(float* x, int64_t x_ld, const float* add, const float* gamma, const float* beta, int B, int d,
+                     void* y, int64_t y_ld, void* stream) {
+  if (B < 1 || d < 4 || d % 4 || d > 4 * kLnSlots * kLnThreads || !x || !gamma || !beta || !y || x_ld < d ||
+      y_ld < d || x_ld % 4 || y_ld % 4)
+    return PS_ERR_VALUE;
+  if (((uintptr_t)x % 16) || ((uintptr_t)gamma % 16) || ((uintptr_t)beta % 16) || ((uintptr_t)y % 8) ||
+      (add && ((uintptr_t)add % 16)))
+    return PS_ERR_VALUE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (add)
+    layernorm_kernel<true><<<B, kLnThreads, 0, st>>>(x, x_ld, add, gamma, beta, d, static_cast<uint16_t*>(y), y_ld);
+  else
+    layernorm_kernel<false><<<B, kLnThreads, 0, st>>>(x, x_ld, nullptr, gamma, beta, d, static_cast<uint16_t*>(y),
+                                                      y_ld);
+  return launch_status();
+}
+
 extern "C" int ps_layernorm(const float* x, int64_t x_ld, const float* gamma, const float* beta, int B, int d,
                             void* y, int64_t y_ld, void* stream) {
-  if (B < 1 || d < 1 || !x || !gamma || !beta || !y || x_ld < d || y_ld < d) return PS_ERR_VALUE;
-  layernorm_kernel<<<B, kLnThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, x_ld, gamma, beta, d,
-                                                                            static_cast<uint16_t*>(y), y_ld);
-  return launch_status();
+  return ln_launch(const_cast<float*>(x), x_ld, nullptr, gamma, beta, B, d, y, y_ld, stream);
+}
+
+extern "C" int ps_add_layernorm(float* x, int64_t x_ld, const float* add, const float* gamma, const float* beta,
+                                int B, int d, void* y, int64_t y_ld, void* stream) {
+  return ln_launch(x, x_ld, add, gamma, beta, B, d, y, y_ld, stream);
 }
 
 extern "C" int ps_embed(const int32_t* tokens, const int32_t* lengths, const void* embed, const void* pos_embed,

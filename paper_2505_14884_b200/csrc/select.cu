@@ -45,78 +45,184 @@ PS_DEV int block_excl_scan(int v, int* s_warp, int* total) {
   return before + x - v;
 }
 
-constexpr int kTopkThreads = 512;
+constexpr int kTopkThreads = 1024;
 constexpr int kTopkWarps = kTopkThreads / 32;
-constexpr int kTopkSmemCols = 49152;  // rows up to this width are staged in shared memory
+constexpr int kTopkSmemCols = 40960;  // rows up to this width are staged in shared memory (160 KB)
+constexpr int kSample = 2048;         // strided sample of a row that brackets the k-th key
+constexpr int kMaxCand = 3072;        // keys inside the bracket kept for the exact select
+constexpr int kGroupRows = 16;        // union: rows ORed by the last CTA of each row group
 
 struct TopkParams {
   const float* logits;
   int rows, cols;
   int64_t ld;
-  int k;            // > 0: top-k per row; <= 0: threshold selection (logit > thr)
+  int k;             // > 0: top-k per row; <= 0: threshold selection (logit > thr)
   float thr;
   int32_t* idx_out;  // (rows, k) ascending ids, or NULL
-  uint32_t* bitmap;  // union bitmap (atomic OR), or NULL
-  // fused union compaction by the last CTA (ticket != NULL)
-  int* ticket;
+  uint32_t* bitmap;  // atomic-OR union bitmap, or NULL
+  // fused union (ps_select_union): per-row words, per-group words, tickets
+  uint32_t* row_bits;    // (rows, words) or NULL
+  uint32_t* group_bits;  // (groups, words)
+  int* tickets;          // [groups] + [1] (self-resetting)
   int lo, hi, pad;
   int32_t* union_out;
   int32_t* count_out;
+  unsigned long long* trace;  // debug phase stamps (16 per CTA) or NULL
 };
 
-// Last-CTA compaction of bitmap bits in [lo, hi) -> ascending ids - lo;
-// clears the whole bitmap.  Called by every thread of one CTA.
+PS_DEV void hist_add_agg(int* hist, bool act, uint32_t bin, int lane) {
+  if (__ballot_sync(0xffffffffu, act)) {
+    const uint32_t b = act ? bin : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    if (act && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&hist[b], __popc(peers));
+  }
+}
+
+// Descending scan of g[0, bins): the bin holding the `remaining`-th largest
+// key.  Writes s_sel = {bin, remaining within the bin, bin count}.
 template <int NT>
-PS_DEV void compact_bitmap(uint32_t* bitmap, int width, int lo, int hi, int pad, int32_t* out, int32_t* count,
-                           int* s_warp) {
-  const int words = (width + 31) >> 5;
+PS_DEV void select_bin(const int* g, int bins, int remaining, int* s_warp, int* s_sel) {
+  const int per = bins / NT;
+  const int hi = bins - (int)threadIdx.x * per;
+  int loc = 0;
+  for (int j = 1; j <= per; ++j) loc += g[hi - j];
+  const int above = block_excl_scan<NT>(loc, s_warp, nullptr);
+  if (above < remaining && above + loc >= remaining) {
+    int cum = above;
+    for (int j = 1; j <= per; ++j) {
+      const int c = g[hi - j];
+      if (cum + c >= remaining) {
+        s_sel[0] = hi - j;
+        s_sel[1] = remaining - cum;
+        s_sel[2] = c;
+        break;
+      }
+      cum += c;
+    }
+  }
+  __syncthreads();
+}
+
+// r-th largest (1-based) of n u32 keys in shared memory: 3 radix passes
+// (12/10/10 bits).  Returns the key; *eq = how many keys equal it, *rem =
+// how many of those reach rank r.  Block-wide; r in [1, n].
+template <int NT>
+PS_DEV uint32_t list_select(const uint32_t* keys, int n, int r, int* hist, int* s_warp, int* s_sel, int* eq,
+                            int* rem) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = 0, mask = 0;
+  int remaining = r;
+#pragma unroll 1
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = pass == 0 ? 20 : (pass == 1 ? 10 : 0);
+    const int bins = pass == 0 ? 4096 : 1024;
+    for (int i = threadIdx.x; i < bins; i += NT) hist[i] = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += NT) {
+      const int i = base + (int)threadIdx.x;
+      const uint32_t u = i < n ? keys[i] : 0u;
+      hist_add_agg(hist, i < n && (u & mask) == prefix, (u >> shift) & (uint32_t)(bins - 1), lane);
+    }
+    __syncthreads();
+    select_bin<NT>(hist, bins, remaining, s_warp, s_sel);
+    prefix |= (uint32_t)s_sel[0] << shift;
+    remaining = s_sel[1];
+    mask |= (uint32_t)(bins - 1) << shift;
+  }
+  *eq = s_sel[2];
+  *rem = remaining;
+  __syncthreads();  // s_sel is reused by the caller
+  return prefix;
+}
+
+// debug: per-CTA globaltimer stamps of the phases (ps_debug_topk_trace)
+PS_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TK_STAMP(slot) \
+  do { if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (slot)] = gtime(); } while (0)
+
+// words [w0, w1) of the OR over `nrows` bitmaps (stride `words`), plain loads
+PS_DEV uint32_t or_rows(const uint32_t* bits, int nrows, int words, int w) {
+  uint32_t acc = 0;
+#pragma unroll 4
+  for (int r = 0; r < nrows; ++r) acc |= __ldcg(bits + (size_t)r * words + w);
+  return acc;
+}
+
+// Ascending ids - lo of the set bits of `word(w)` in [lo, hi); device count;
+// idx_out padded up to a multiple of `pad` with the last id.
+template <int NT, typename WordFn>
+PS_DEV void compact_words(WordFn word, int lo, int hi, int pad, int32_t* out, int32_t* count, int* s_warp) {
   const int wlo = lo >> 5, whi = (hi + 31) >> 5;
   const int nw = whi - wlo;
   const int per = (nw + NT - 1) / NT;
   const int w0 = wlo + min(nw, (int)threadIdx.x * per), w1 = wlo + min(nw, (int)(threadIdx.x + 1) * per);
-  auto word = [&](int w) {
-    uint32_t bits = __ldcg(bitmap + w);
+  auto clip = [&](int w, uint32_t bits) {
     const int top = hi - (w << 5);
     if (top < 32) bits &= (top <= 0) ? 0u : ((1u << top) - 1u);
     return bits;
   };
+  uint32_t mine[4];
   int cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(word(w));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    mine[j] = (w0 + j < w1) ? clip(w0 + j, word(w0 + j)) : 0u;
+    cnt += __popc(mine[j]);
+  }
+  for (int w = w0 + 4; w < w1; ++w) cnt += __popc(clip(w, word(w)));
   int total;
   int pos = block_excl_scan<NT>(cnt, s_warp, &total);
   for (int w = w0; w < w1; ++w) {
-    uint32_t bits = word(w);
+    uint32_t bits = (w - w0 < 4) ? mine[w - w0] : clip(w, word(w));
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       out[pos++] = (w << 5) + b - lo;
     }
   }
-  __syncthreads();
-  for (int w = threadIdx.x; w < words; w += NT) bitmap[w] = 0u;
   if (threadIdx.x == 0) *count = total;
   if (pad > 1) {
-    const int padded = (total + pad - 1) / pad * pad;
     __syncthreads();
+    const int padded = (total + pad - 1) / pad * pad;
     const int32_t last = total > 0 ? out[total - 1] : 0;
-    for (int i = total + threadIdx.x; i < padded; i += NT) out[i] = last;
+    for (int i = total + (int)threadIdx.x; i < padded; i += NT) out[i] = last;
   }
 }
 
-// One CTA per row.  Top-k: 3-pass (12/10/10-bit) radix select of the k-th
-// largest key over keys staged in shared memory, then ONE index-order pass in which each
-// warp owns a contiguous segment and ranks its elements with ballots: keep
-// every key above the k-th and the lowest-index ties up to k (exactly the
-// stable-argsort rule).  Threshold mode keeps logit > thr.  Each 32-id word
-// of the selection is ORed into the union bitmap once, by one lane.
+// Per-row top-k (and threshold selection), bit-exact with numpy's stable
+// argsort of -scores: value descending, ties -> lower index, -0.0 == +0.0,
+// NaN below -inf.  One CTA (1024 threads) per row; the row is staged in
+// shared memory as order-preserving u32 keys.
+//   1. bracket: a strided sample of 2048 keys, taken while staging, gives
+//      the sample order statistics at ranks k*S/cols -/+ (3 sigma + 2) to
+//      22-bit precision (two shared radix passes);
+//   2. one pass counts the keys above the bracket and appends the keys
+//      inside it (~7 % of the row) to a candidate list;
+//   3. exact k-th key T = radix select over the candidates; ties at T go to
+//      the lowest columns: the last one taken, I, is a radix select over the
+//      tied candidates' inverted columns;
+//   4. every key is then decided locally (key > T, or key == T and column
+//      <= I): one ballot per 32 columns.
+// The bracket is verified exactly (count above < k <= above + candidates);
+// a miss falls back to a full 3-pass radix select with per-warp tie ranking.
+// Outputs: ids (ps_topk_rows), an atomic-OR bitmap, or -- ps_select_union --
+// this row's words stored plainly; the last CTA of each group of 16 rows ORs
+// the group, and the last group compacts the union (ascending ids, device
+// count, padded): no contended atomics.  Threshold mode keeps logit > thr.
 __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  int* hist = reinterpret_cast<int*>(smem);                              // [4096] radix histogram
-  uint32_t* keys = reinterpret_cast<uint32_t*>(hist + 4096);              // [cols] if staged
+  int* hist = reinterpret_cast<int*>(smem);                          // [4096]
+  uint32_t* samp = reinterpret_cast<uint32_t*>(hist + 4096);         // [kMaxCand] samples, then tied cols
+  uint32_t* cand_key = samp + kMaxCand;                              // [kMaxCand]
+  int* cand_idx = reinterpret_cast<int*>(cand_key + kMaxCand);       // [kMaxCand]
+  uint32_t* keys = reinterpret_cast<uint32_t*>(cand_idx + kMaxCand);  // [cols] if staged
   __shared__ int s_warp[32];
   __shared__ int s_eq[kTopkWarps], s_gt[kTopkWarps];
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_remaining, s_last;
+  __shared__ int s_sel[3];
+  __shared__ int s_nc, s_na, s_n2, s_last;
   const int row = blockIdx.x, cols = p.cols;
   const float* x = p.logits + (size_t)row * p.ld;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -124,72 +230,186 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   const bool staged = !threshold && cols <= kTopkSmemCols;
   auto key_at = [&](int i) -> uint32_t { return staged ? keys[i] : order_key(__ldg(x + i)); };
 
+  TK_STAMP(0);
   uint32_t prefix = 0;
   int remaining = 0;
+  bool fast = true;          // every key decided locally
+  int tie_lim = 0x7fffffff;  // fast: tied keys at column < tie_lim are taken
   if (!threshold) {
-    if (staged)
-      for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(__ldg(x + i));
-    // three radix passes over (12, 10, 10) key bits; only keys matching the
-    // prefix found so far touch the histogram, so after the first pass
-    // (where the exponent clustering of real logits spreads over ~10^2
-    // bins) almost no atomics are issued
-    remaining = p.k;
-    uint32_t mask = 0;
-    const int shifts[3] = {20, 10, 0};
-    const int nbins[3] = {4096, 1024, 1024};
-#pragma unroll 1
-    for (int pass = 0; pass < 3; ++pass) {
-      const int shift = shifts[pass], bins = nbins[pass];
-      for (int i = tid; i < bins; i += kTopkThreads) hist[i] = 0;
-      __syncthreads();
-      for (int i = tid; i < cols; i += kTopkThreads) {
-        const uint32_t u = key_at(i);
-        if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & (uint32_t)(bins - 1)], 1);
-      }
-      __syncthreads();
-      // descending scan: thread t owns bins [bins - (t+1)*per, bins - t*per)
-      const int per = bins / kTopkThreads;  // 8 or 2
-      const int hi = bins - tid * per;
-      int loc = 0;
-      for (int j = 1; j <= per; ++j) loc += hist[hi - j];
-      const int above = block_excl_scan<kTopkThreads>(loc, s_warp, nullptr);
-      if (above < remaining && above + loc >= remaining) {
-        int cum = above;
-        for (int j = 1; j <= per; ++j) {
-          const int c = hist[hi - j];
-          if (cum + c >= remaining) {
-            s_prefix = prefix | ((uint32_t)(hi - j) << shift);
-            s_remaining = remaining - cum;
-            break;
-          }
-          cum += c;
+    if (tid == 0) { s_nc = 0; s_na = 0; s_n2 = 0; }
+    for (int i = tid; i < 4096; i += kTopkThreads) hist[i] = 0;
+    // ---- stage the keys, keep a strided sample
+    const int S = min(cols, kSample);
+    const int stride = cols / S;
+    if (staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0) {
+      const float4* x4 = reinterpret_cast<const float4*>(x);
+      for (int i = tid; i < (cols >> 2); i += kTopkThreads) {
+        const float4 v = __ldg(x4 + i);
+        const uint4 u = make_uint4(order_key(v.x), order_key(v.y), order_key(v.z), order_key(v.w));
+        *reinterpret_cast<uint4*>(keys + 4 * i) = u;
+        const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int e = 4 * i + j;
+          if (e % stride == 0 && e / stride < S) samp[e / stride] = uu[j];
         }
       }
-      __syncthreads();
-      prefix = s_prefix;
-      remaining = s_remaining;
-      mask |= (uint32_t)(bins - 1) << shift;
-      __syncthreads();
+    } else {
+      if (staged)
+        for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(__ldg(x + i));
+      for (int j = tid; j < S; j += kTopkThreads) samp[j] = order_key(__ldg(x + (size_t)j * stride));
+    }
+    __syncthreads();
+    TK_STAMP(1);
+    // ---- 1. bracket: sample order statistics at 22-bit precision
+    const float q = (float)p.k / (float)cols;
+    const float rs = q * (float)S;
+    const float dl = 3.f * sqrtf(fmaxf(rs * (1.f - q), 0.f)) + 2.f;
+    const bool open_top = rs - dl < 1.f, open_bottom = rs + dl > (float)S;
+    const int r_hi = max(1, min(S, (int)floorf(rs - dl)));
+    const int r_lo = max(1, min(S, (int)ceilf(rs + dl)));
+    for (int base = 0; base < S; base += kTopkThreads) {
+      const int j = base + tid;
+      const uint32_t u = j < S ? samp[j] : 0u;
+      hist_add_agg(hist, j < S, u >> 20, lane);
+    }
+    __syncthreads();
+    select_bin<kTopkThreads>(hist, 4096, r_hi, s_warp, s_sel);
+    const int bin_hi = s_sel[0], rem_hi = s_sel[1];
+    select_bin<kTopkThreads>(hist, 4096, r_lo, s_warp, s_sel);
+    const int bin_lo = s_sel[0], rem_lo = s_sel[1];
+    for (int i = tid; i < 2048; i += kTopkThreads) hist[i] = 0;
+    __syncthreads();
+    for (int base = 0; base < S; base += kTopkThreads) {
+      const int j = base + tid;
+      const uint32_t u = j < S ? samp[j] : 0u;
+      const int top = (int)(u >> 20);
+      const uint32_t sub = (u >> 10) & 1023u;
+      hist_add_agg(hist, j < S && top == bin_hi, sub, lane);
+      hist_add_agg(hist + 1024, j < S && top == bin_lo, sub, lane);
+    }
+    __syncthreads();
+    select_bin<kTopkThreads>(hist, 1024, rem_hi, s_warp, s_sel);
+    const uint32_t hi22 = open_top ? 0x3FFFFFu : (((uint32_t)bin_hi << 10) | (uint32_t)s_sel[0]);
+    select_bin<kTopkThreads>(hist + 1024, 1024, rem_lo, s_warp, s_sel);
+    const uint32_t lo22 = open_bottom ? 0u : (((uint32_t)bin_lo << 10) | (uint32_t)s_sel[0]);
+    TK_STAMP(2);
+    // ---- 2. count above / collect candidates
+    {
+      int n_above = 0;
+      for (int base = 0; base < cols; base += kTopkThreads) {
+        const int i = base + tid;
+        const uint32_t u = i < cols ? key_at(i) : 0u;
+        const uint32_t t22 = u >> 10;
+        const bool above = i < cols && t22 > hi22;
+        const bool cand = i < cols && t22 >= lo22 && t22 <= hi22;
+        n_above += __popc(__ballot_sync(0xffffffffu, above));
+        const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+        if (bal) {
+          const int leader = __ffs(bal) - 1;
+          int slot = 0;
+          if (lane == leader) slot = atomicAdd(&s_nc, __popc(bal));
+          slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(bal & ((1u << lane) - 1u));
+          if (cand && slot < kMaxCand) {
+            cand_key[slot] = u;
+            cand_idx[slot] = i;
+          }
+        }
+      }
+      if (lane == 0) atomicAdd(&s_na, n_above);
+    }
+    __syncthreads();
+    TK_STAMP(3);
+    const int n_above = s_na, n_cand = s_nc;
+    if (n_above < p.k && n_above + n_cand >= p.k && n_cand <= kMaxCand) {
+      // ---- 3. exact k-th key among the candidates, then the tie column
+      int n_eq, rem;
+      prefix = list_select<kTopkThreads>(cand_key, n_cand, p.k - n_above, hist, s_warp, s_sel, &n_eq, &rem);
+      remaining = rem;
+      if (rem < n_eq) {
+        for (int base = 0; base < n_cand; base += kTopkThreads) {
+          const int j = base + tid;
+          const bool eq = j < n_cand && cand_key[j] == prefix;
+          const uint32_t bal = __ballot_sync(0xffffffffu, eq);
+          if (bal) {
+            const int leader = __ffs(bal) - 1;
+            int slot = 0;
+            if (lane == leader) slot = atomicAdd(&s_n2, __popc(bal));
+            slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(bal & ((1u << lane) - 1u));
+            if (eq) samp[slot] = ~(uint32_t)cand_idx[j];  // descending ~col == ascending col
+          }
+        }
+        __syncthreads();
+        int e2, r2;
+        const uint32_t v = list_select<kTopkThreads>(samp, s_n2, rem, hist, s_warp, s_sel, &e2, &r2);
+        tie_lim = (int)~v + 1;  // the highest taken tied column + 1
+      }
+      if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 10] = ((unsigned long long)n_cand << 32) | (unsigned)n_eq;
+    } else {
+      // ---- fallback: full radix select over all keys
+      if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 11] = 1;
+      remaining = p.k;
+      uint32_t mask = 0;
+#pragma unroll 1
+      for (int pass = 0; pass < 3; ++pass) {
+        const int shift = pass == 0 ? 20 : (pass == 1 ? 10 : 0);
+        const int bins = pass == 0 ? 4096 : 1024;
+        for (int i = tid; i < bins; i += kTopkThreads) hist[i] = 0;
+        __syncthreads();
+        for (int base = 0; base < cols; base += kTopkThreads) {
+          const int i = base + tid;
+          const uint32_t u = i < cols ? key_at(i) : 0u;
+          hist_add_agg(hist, i < cols && (u & mask) == prefix, (u >> shift) & (uint32_t)(bins - 1), lane);
+        }
+        __syncthreads();
+        select_bin<kTopkThreads>(hist, bins, remaining, s_warp, s_sel);
+        prefix |= (uint32_t)s_sel[0] << shift;
+        remaining = s_sel[1];
+        mask |= (uint32_t)(bins - 1) << shift;
+      }
+      if (s_sel[2] != remaining) fast = false;  // rank ties with per-warp counts
     }
   }
+  TK_STAMP(4);
 
-  // ---- index-order selection: warp-contiguous segments (multiples of 32)
-  const int seg = (cols + kTopkThreads - 1) / kTopkThreads * 32;
-  const int sbeg = warp * seg, send = min(cols, sbeg + seg);
-  auto classify = [&](int e, bool& gt, bool& eq) {
-    gt = eq = false;
-    if (e < send) {
-      if (threshold) {
-        gt = __ldg(x + e) > p.thr;
-      } else {
-        const uint32_t u = key_at(e);
-        gt = u > prefix;
-        eq = u == prefix;
+  // ---- 4. selection
+  const int words = (cols + 31) >> 5;
+  if (fast && !p.idx_out) {
+    // decide, ballot, store / OR the word
+    for (int w = warp; w < words; w += kTopkWarps) {
+      const int e = (w << 5) + lane;
+      bool take = false;
+      if (e < cols) {
+        if (threshold) {
+          take = __ldg(x + e) > p.thr;
+        } else {
+          const uint32_t u = key_at(e);
+          take = u > prefix || (u == prefix && e < tie_lim);
+        }
+      }
+      const uint32_t bt = __ballot_sync(0xffffffffu, take);
+      if (lane == 0) {
+        if (p.row_bits) p.row_bits[(size_t)row * words + w] = bt;
+        else if (p.bitmap && bt) atomicOr(p.bitmap + w, bt);
       }
     }
-  };
-  int n_eq = 0, n_gt = 0;
-  if (!threshold || p.idx_out) {
+  } else {
+    // index-order: warp-contiguous segments (multiples of 32)
+    const int seg = (cols + kTopkThreads - 1) / kTopkThreads * 32;
+    const int sbeg = warp * seg, send = min(cols, sbeg + seg);
+    auto classify = [&](int e, bool& gt, bool& eq) {
+      gt = eq = false;
+      if (e < send) {
+        const uint32_t u = key_at(e);
+        if (fast) {
+          gt = u > prefix || (u == prefix && e < tie_lim);
+        } else {
+          gt = u > prefix;
+          eq = u == prefix;
+        }
+      }
+    };
+    int n_eq = 0, n_gt = 0;
     for (int e0 = sbeg; e0 < send; e0 += 32) {
       bool gt, eq;
       classify(e0 + lane, gt, eq);
@@ -201,49 +421,70 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       s_gt[warp] = n_gt;
     }
     __syncthreads();
-  }
-  int eq_before = 0, gt_before = 0;
-  if (!threshold || p.idx_out)
+    int eq_before = 0, gt_before = 0;
     for (int w = 0; w < warp; ++w) {
       eq_before += s_eq[w];
       gt_before += s_gt[w];
     }
-  int pos = gt_before + (threshold ? 0 : min(eq_before, remaining));
-  int eq_run = eq_before;
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int e0 = sbeg; e0 < send; e0 += 32) {
-    bool gt, eq;
-    classify(e0 + lane, gt, eq);
-    const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-    const bool take = gt || (eq && (eq_run + __popc(beq & lt)) < remaining);
-    const uint32_t bt = __ballot_sync(0xffffffffu, take);
-    eq_run += __popc(beq);
-    if (take && p.idx_out) p.idx_out[(size_t)row * p.k + pos + __popc(bt & lt)] = e0 + lane;
-    pos += __popc(bt);
-    if (p.bitmap && lane == 0 && bt) atomicOr(p.bitmap + (e0 >> 5), bt);
+    int pos = gt_before + (fast ? 0 : min(eq_before, remaining));
+    int eq_run = eq_before;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int e0 = sbeg; e0 < send; e0 += 32) {
+      bool gt, eq;
+      classify(e0 + lane, gt, eq);
+      const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+      const bool take = gt || (eq && (eq_run + __popc(beq & lt)) < remaining);
+      const uint32_t bt = __ballot_sync(0xffffffffu, take);
+      eq_run += __popc(beq);
+      if (take && p.idx_out) p.idx_out[(size_t)row * p.k + pos + __popc(bt & lt)] = e0 + lane;
+      pos += __popc(bt);
+      if (lane == 0) {
+        if (p.row_bits) p.row_bits[(size_t)row * words + (e0 >> 5)] = bt;
+        else if (p.bitmap && bt) atomicOr(p.bitmap + (e0 >> 5), bt);
+      }
+    }
   }
+  TK_STAMP(5);
 
-  // ---- fused union compaction by the last CTA
-  if (p.ticket) {
+  // ---- fused union: group OR by the last CTA of each row group, then the
+  //      last group compacts
+  if (p.row_bits) {
+    const int groups = (p.rows + kGroupRows - 1) / kGroupRows;
+    const int g = row / kGroupRows;
+    const int g_rows = min(kGroupRows, p.rows - g * kGroupRows);
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(p.ticket, 1) == (int)gridDim.x - 1;
+    if (tid == 0) s_last = atomicAdd(&p.tickets[g], 1) == g_rows - 1;
     __syncthreads();
-    if (s_last) {
-      __threadfence();
-      compact_bitmap<kTopkThreads>(p.bitmap, cols, p.lo, p.hi, p.pad, p.union_out, p.count_out, s_warp);
-      if (tid == 0) *p.ticket = 0;
-    }
+    if (!s_last) return;
+    __threadfence();
+    const uint32_t* gb = p.row_bits + (size_t)g * kGroupRows * words;
+    for (int w = tid; w < words; w += kTopkThreads) p.group_bits[(size_t)g * words + w] = or_rows(gb, g_rows, words, w);
+    if (tid == 0) p.tickets[g] = 0;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&p.tickets[groups], 1) == groups - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const uint32_t* gbits = p.group_bits;
+    compact_words<kTopkThreads>([&](int w) { return or_rows(gbits, groups, words, w); }, p.lo, p.hi, p.pad,
+                                p.union_out, p.count_out, s_warp);
+    if (tid == 0) p.tickets[groups] = 0;
+    TK_STAMP(6);
   }
 }
 
 size_t topk_smem(int cols, bool threshold) {
-  size_t b = (size_t)4096 * 4;
+  size_t b = (size_t)4096 * 4 + (size_t)kMaxCand * 4 * 3;
   if (!threshold && cols <= kTopkSmemCols) b += (size_t)cols * 4;
   return b;
 }
 
-int launch_topk(const TopkParams& prm, cudaStream_t st) {
+unsigned long long* g_topk_trace = nullptr;
+
+int launch_topk(TopkParams prm, cudaStream_t st) {
+  prm.trace = g_topk_trace;
   const size_t smem = topk_smem(prm.cols, prm.k <= 0);
   static int configured = 0;
   if (!configured) {
@@ -311,57 +552,102 @@ __global__ void __launch_bounds__(kCompactThreads) bitmap_compact_kernel(uint32_
   }
 }
 
-// Head router fused with top-k.  R rows per CTA share each 16-byte W^T load.
+// Head router fused with top-k (routers.py:324-325 + tensors.py:65-73).
+// One thread-block CLUSTER per group of R batch rows: CTA j of the cluster
+// computes the logits of heads [j*HB, (j+1)*HB) for those rows (each warp
+// one (head, d-segment) item, all of a lane's 16-byte W^T loads independent
+// so they are in flight together), and stores them into CTA 0's shared
+// memory through DSMEM; after one cluster barrier CTA 0 ranks every row
+// (one warp per row).  The whole W^T (H x d bf16) is read once per cluster,
+// from L2 after the first cluster.
 constexpr int kHrThreads = 256;
-constexpr int kHrRows = 1;
+constexpr int kHrWarps = kHrThreads / 32;
 constexpr int kHrMaxHeads = 256;
+constexpr int kHrMaxRows = 4;
 
+template <int R>
 __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
     const uint16_t* __restrict__ x, int64_t x_ld, const uint16_t* __restrict__ w_t, const float* __restrict__ bias,
-    int B, int d, int H, int k, float* __restrict__ logits_out, int32_t* __restrict__ sel_out) {
+    int B, int d, int H, int HB, int k, float* __restrict__ logits_out, int32_t* __restrict__ sel_out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint16_t* sx = reinterpret_cast<uint16_t*>(smem);                       // [kHrRows][d]
-  float* slog = reinterpret_cast<float*>(smem + (size_t)kHrRows * d * 2);  // [kHrRows][H]
-  const int r0 = blockIdx.x * kHrRows;
-  const int nr = min(kHrRows, B - r0);
+  __shared__ float s_log[kHrMaxRows * kHrMaxHeads];          // CTA 0: the cluster's logits
+  __shared__ float s_part[kHrWarps * 2][kHrMaxRows];         // per-item partial sums
+  uint16_t* sx = reinterpret_cast<uint16_t*>(smem);          // [R][d]
+  const int crank = (int)cluster_rank(), csize = (int)cluster_size();
+  const int r0 = (blockIdx.x / csize) * R;
+  const int nr = min(R, B - r0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int chunks = d / 8;
-  for (int c = tid; c < kHrRows * chunks; c += kHrThreads) {
+  const int chunks = d >> 3;
+  // every CTA of the cluster must have started before its DSMEM is written
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  for (int c = tid; c < R * chunks; c += kHrThreads) {
     const int r = c / chunks, cc = c - r * chunks;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < nr) v = *reinterpret_cast<const uint4*>(x + (size_t)(r0 + r) * x_ld + cc * 8);
     *reinterpret_cast<uint4*>(sx + r * d + cc * 8) = v;
   }
+  const int h0 = crank * HB;
+  const int hn = max(0, min(HB, H - h0));
+  // items = (head, segment); segments per head so that every warp has work
+  const int segs = hn > 0 ? max(1, kHrWarps / hn) : 1;
+  const int items = hn * segs;
+  const int seg_len = (chunks + segs - 1) / segs;
   __syncthreads();
-  for (int h = warp; h < H; h += kHrThreads / 32) {
-    float acc[kHrRows];
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  const uint32_t s_log_base = smem_u32(s_log);
+  const uint32_t leader_log = map_peer(s_log_base, 0);
+  for (int it0 = 0; it0 < items; it0 += kHrWarps) {
+    const int it = it0 + warp;
+    if (it < items) {
+      const int hh = it / segs, sg = it - hh * segs;
+      const int c0 = sg * seg_len, c1 = min(chunks, c0 + seg_len);
+      const uint16_t* wr = w_t + (size_t)(h0 + hh) * d;
+      float acc[R];
 #pragma unroll
-    for (int r = 0; r < kHrRows; ++r) acc[r] = 0.f;
-    for (int cc = lane; cc < chunks; cc += 32) {
-      float wf[8], xf[8];
-      unpack8(*reinterpret_cast<const uint4*>(w_t + (size_t)h * d + cc * 8), wf);
+      for (int r = 0; r < R; ++r) acc[r] = 0.f;
+#pragma unroll 8
+      for (int c = c0 + lane; c < c1; c += 32) {
+        float wf[8], xf[8];
+        unpack8(__ldg(reinterpret_cast<const uint4*>(wr + c * 8)), wf);
 #pragma unroll
-      for (int r = 0; r < kHrRows; ++r) {
-        unpack8(*reinterpret_cast<const uint4*>(sx + r * d + cc * 8), xf);
+        for (int r = 0; r < R; ++r) {
+          unpack8(*reinterpret_cast<const uint4*>(sx + r * d + c * 8), xf);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[r] = fmaf(wf[i], xf[i], acc[r]);
+          for (int i = 0; i < 8; ++i) acc[r] = fmaf(wf[i], xf[i], acc[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float v = warp_sum(acc[r]);
+        if (lane == 0) s_part[warp][r] = v;
       }
     }
-#pragma unroll
-    for (int r = 0; r < kHrRows; ++r) {
-      float v = warp_sum(acc[r]);
-      if (lane == 0) slog[r * H + h] = v + (bias ? bias[h] : 0.f);
+    __syncthreads();
+    // combine the segments of each head of this round; ship to CTA 0
+    const int n_round = min(kHrWarps, items - it0);
+    if (tid < R * kHrWarps) {
+      const int r = tid / kHrWarps, j = tid - r * kHrWarps;  // j: item slot in this round
+      if (j < n_round && r < nr) {
+        const int item = it0 + j, hh = item / segs, sg = item - hh * segs;
+        if (sg == 0) {
+          float v = 0.f;
+          for (int q = 0; q < segs; ++q) v += s_part[j + q][r];  // segments of a head are adjacent slots
+          const int h = h0 + hh;
+          v += bias ? bias[h] : 0.f;
+          st_dsmem_f32(leader_log + (uint32_t)(r * H + h) * 4u, v);
+        }
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  // top-k of each row by rank counting (H <= kHrMaxHeads), one warp per row
+  cluster_sync_all();
+  if (crank != 0) return;
+  // top-k of each row by rank counting, one warp per row
   if (warp < nr) {
     const int r = warp;
-    const float* lr = slog + r * H;
-    for (int i = lane; i < H; i += 32) {
-      if (logits_out) logits_out[(size_t)(r0 + r) * H + i] = lr[i];
-    }
-    // selected flags -> ascending positions
+    const float* lr = s_log + r * H;
+    if (logits_out)
+      for (int i = lane; i < H; i += 32) logits_out[(size_t)(r0 + r) * H + i] = lr[i];
     int base = 0;
     for (int i0 = 0; i0 < H; i0 += 32) {
       const int i = i0 + lane;
@@ -380,6 +666,37 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
       base += __popc(ballot);
     }
   }
+}
+
+template <int R>
+int launch_head_router(const uint16_t* x, int64_t x_ld, const uint16_t* w_t, const float* bias, int B, int d,
+                       int H, int k, float* logits_out, int32_t* sel_out, cudaStream_t st) {
+  auto kern = head_router_topk_kernel<R>;
+  const size_t smem = (size_t)R * d * 2;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024) != cudaSuccess)
+      return PS_ERR_CUDA;
+    configured = true;
+  }
+  const int csize = H < 8 ? H : 8;
+  const int HB = (H + csize - 1) / csize;
+  const int groups = (B + R - 1) / R;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(groups * csize);
+  cfg.blockDim = dim3(kHrThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, x, x_ld, w_t, bias, B, d, H, HB, k, logits_out, sel_out) != cudaSuccess)
+    return PS_ERR_CUDA;
+  return launch_status();
 }
 
 }  // namespace
@@ -406,18 +723,37 @@ extern "C" int ps_threshold_rows(const float* logits, int rows, int cols, int64_
   return launch_topk(prm, static_cast<cudaStream_t>(stream));
 }
 
-extern "C" int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr,
-                               uint32_t* bitmap, int* ticket, int lo, int hi, int pad, int32_t* union_out,
-                               int32_t* count_out, void* stream) {
-  if (rows < 1 || cols < 1 || ld < cols || k > cols || !logits || !bitmap || !ticket || !union_out || !count_out)
+static size_t su_words(int cols) { return (size_t)(cols + 31) / 32; }
+static size_t su_groups(int rows) { return (size_t)(rows + kGroupRows - 1) / kGroupRows; }
+
+extern "C" size_t ps_select_union_workspace_bytes(int rows, int cols) {
+  if (rows < 1 || cols < 1) return 0;
+  const size_t tickets = (su_groups(rows) + 1) * 4;
+  const size_t head = (tickets + 255) / 256 * 256;
+  return head + (su_groups(rows) + (size_t)rows) * su_words(cols) * 4;
+}
+
+extern "C" int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr, void* ws,
+                               size_t ws_bytes, int lo, int hi, int pad, int32_t* union_out, int32_t* count_out,
+                               void* stream) {
+  if (rows < 1 || cols < 1 || ld < cols || k > cols || !logits || !ws || !union_out || !count_out)
     return PS_ERR_VALUE;
   if (lo < 0 || lo % 32 || hi > cols || hi <= lo || pad < 1) return PS_ERR_VALUE;
+  if (ws_bytes < ps_select_union_workspace_bytes(rows, cols)) return PS_ERR_WORKSPACE;
   TopkParams prm{};
   prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k > 0 ? k : 0; prm.thr = thr;
-  prm.bitmap = bitmap; prm.ticket = ticket; prm.lo = lo; prm.hi = hi; prm.pad = pad;
+  const size_t tickets = (su_groups(rows) + 1) * 4;
+  const size_t head = (tickets + 255) / 256 * 256;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  prm.tickets = reinterpret_cast<int*>(base);
+  prm.group_bits = reinterpret_cast<uint32_t*>(base + head);
+  prm.row_bits = prm.group_bits + su_groups(rows) * su_words(cols);
+  prm.lo = lo; prm.hi = hi; prm.pad = pad;
   prm.union_out = union_out; prm.count_out = count_out;
   return launch_topk(prm, static_cast<cudaStream_t>(stream));
 }
+
+extern "C" void ps_debug_topk_trace(void* buf) { g_topk_trace = static_cast<unsigned long long*>(buf); }
 
 extern "C" int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width, uint32_t* bitmap, void* stream) {
   if (rows < 1 || k < 1 || width < 1 || !rows_idx || !bitmap) return PS_ERR_VALUE;
@@ -441,18 +777,12 @@ extern "C" int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t,
                                    int H_kv, int k, float* logits_out, int32_t* sel_out, void* stream) {
   if (B < 1 || d < 8 || d % 8 || H_kv < 1 || H_kv > kHrMaxHeads || k < 1 || k > H_kv) return PS_ERR_VALUE;
   if (!x || !w_t || !sel_out || x_ld < d || x_ld % 8) return PS_ERR_VALUE;
-  const size_t smem = (size_t)kHrRows * d * 2 + (size_t)kHrRows * H_kv * 4;
-  if (smem > 200 * 1024) return PS_ERR_UNSUPPORTED;
-  static int configured = 0;
-  if (!configured) {
-    if (cudaFuncSetAttribute(head_router_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
-        cudaSuccess)
-      return PS_ERR_CUDA;
-    configured = 1;
-  }
-  const int grid = (B + kHrRows - 1) / kHrRows;
-  head_router_topk_kernel<<<grid, kHrThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint16_t*>(x), x_ld, static_cast<const uint16_t*>(w_t), bias, B, d, H_kv, k, logits_out,
-      sel_out);
-  return launch_status();
+  if ((size_t)kHrMaxRows * d * 2 > 160 * 1024) return PS_ERR_UNSUPPORTED;
+  const auto* xp = static_cast<const uint16_t*>(x);
+  const auto* wp = static_cast<const uint16_t*>(w_t);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // rows per cluster: keep >= ~64 clusters in flight, fewer W^T re-reads at large batch
+  if (B >= 256) return launch_head_router<4>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, st);
+  if (B >= 128) return launch_head_router<2>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, st);
+  return launch_head_router<1>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, st);
 }

@@ -164,8 +164,8 @@ class DecodeEngine:
             h_r = mlp_routers[0].hidden_dim_
             self.r_hid = torch.zeros(batch, h_r, dtype=bf, device=dev)
             self.r_logits = torch.zeros(batch, D, dtype=f32, device=dev)
-            self.bitmap = torch.zeros((D + 31) // 32, dtype=torch.int32, device=dev)
-            self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.su_bytes = int(_lib.load().ps_select_union_workspace_bytes(batch, D))
+            self.su_ws = torch.zeros(self.su_bytes, dtype=torch.uint8, device=dev)
             self.union_idx = torch.zeros(_round_up(D, ROW_PAD), dtype=torch.int32, device=dev)
             self.union_count = torch.zeros(1, dtype=torch.int32, device=dev)
             self.union_counts = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
@@ -228,32 +228,46 @@ class DecodeEngine:
     def _linear_bf16(self, x2d, w_t, bias, out, act_relu=False, tag="gg"):
         """out (bf16) = act(x w^T + bias)."""
         if self.dense_backend == "cublas":
-            if bias is not None:
+            if bias is not None and act_relu:  # cublasLt RELU_BIAS epilogue
+                torch._addmm_activation(self._bf(bias), x2d, w_t.t(), out=out)
+            elif bias is not None:
                 torch.addmm(self._bf(bias), x2d, w_t.t(), out=out)
             else:
                 torch.mm(x2d, w_t.t(), out=out)
-            if act_relu:
-                out.relu_()
+                if act_relu:
+                    out.relu_()
             return 0
         gather_gemm_into(w_t, None, None, x2d, x2d.stride(0), bias, x2d.shape[0], w_t.shape[0], x2d.shape[1],
                          _lib.PS_ACT_RELU if act_relu else _lib.PS_ACT_NONE, out, out.stride(0), tag=tag)
         return 1
 
-    def _linear_f32(self, x2d, w_t, bias, out, residual=False, tag="gg"):
-        """out (f32) = x w^T + bias (+ out if residual)."""
+    def _linear_f32(self, x2d, w_t, bias, out, residual=False, tag="gg", defer_bias=False):
+        """out (f32) = x w^T + bias (+ out if residual).  cuBLAS accumulates
+        the residual in its epilogue (beta = 1).  With ``defer_bias`` the
+        bias is NOT added here: the caller hands it to the next
+        ps_add_layernorm as the pending bias (returned as the 2nd value)."""
         if self.dense_backend == "cublas":
             if residual:
-                tmp = self._scratch(tag, out.shape, torch.float32)
-                torch.mm(x2d, w_t.t(), out_dtype=torch.float32, out=tmp)
-                out.add_(tmp)
+                torch.addmm(out, x2d, w_t.t(), out_dtype=torch.float32, out=out)
+            elif bias is not None and not defer_bias:  # bias in the GEMM epilogue
+                torch.addmm(bias, x2d, w_t.t(), out_dtype=torch.float32, out=out)
+                bias = None
             else:
                 torch.mm(x2d, w_t.t(), out_dtype=torch.float32, out=out)
-            if bias is not None:
+            if bias is not None and not defer_bias:
                 out.add_(bias)
-            return 0
+            return (0, bias) if defer_bias else 0
         gather_gemm_into(w_t, None, None, x2d, x2d.stride(0), bias, x2d.shape[0], w_t.shape[0], x2d.shape[1],
                          _lib.PS_ACT_NONE, out, out.stride(0), residual=out if residual else None,
                          res_ld=out.stride(0), tag=tag)
+        return (1, None) if defer_bias else 1
+
+    def _ln(self, g, b, pending) -> int:
+        """h = layernorm(x (+= pending bias)) -- ps_add_layernorm."""
+        d = self.cfg.model_dim
+        _lib.check(_lib.load().ps_add_layernorm(_lib.ptr(self.x), d, _lib.ptr(pending) if pending is not None else None,
+                                                _lib.ptr(g), _lib.ptr(b), self.B, d, _lib.ptr(self.h), d,
+                                                _lib.stream_ptr()), "ps_add_layernorm")
         return 1
 
     def step_launches(self) -> int:
@@ -268,11 +282,11 @@ class DecodeEngine:
                               _lib.ptr(m.pos_embed), B, d, _lib.ptr(self.x), st), "ps_embed")
         n += 1
         qkv_w = self.qkv.shape[1]
+        pending = None  # bias of the last residual GEMM, folded into the next LN
         for ell, lw in enumerate(m.layers):
             c = self.caches[ell]
-            _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(lw.ln1_g), _lib.ptr(lw.ln1_b), B, d,
-                                      _lib.ptr(self.h), d, st), "ps_layernorm")
-            n += 1
+            n += self._ln(lw.ln1_g, lw.ln1_b, pending)
+            pending = None
             n += self._linear_bf16(self.h, lw.w_qkv_t, lw.b_qkv, self.qkv, tag="gg_qkv")
             kq = self.qkv[:, self.d_loc:]
             vq = self.qkv[:, self.d_loc + self.dk_loc:]
@@ -299,12 +313,13 @@ class DecodeEngine:
                             group_base=self.group_base, max_len_hint=int(c.host_lengths.max()) + 1)
             n += 1
             if self.tp is None:
-                n += self._linear_f32(self.attn, lw.w_o_t, lw.b_o, self.x, residual=True, tag="gg_o")
+                k, pending = self._linear_f32(self.attn, lw.w_o_t, lw.b_o, self.x, residual=True, tag="gg_o",
+                                              defer_bias=True)
+                n += k
             else:
                 n += self.tp.o_proj(self, lw)
-            _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(lw.ln2_g), _lib.ptr(lw.ln2_b), B, d,
-                                      _lib.ptr(self.h), d, st), "ps_layernorm")
-            n += 1
+            n += self._ln(lw.ln2_g, lw.ln2_b, pending)
+            pending = None
             if self.sparse_mlp:
                 r = self.mlp_routers[ell]
                 if self.dense_backend == "cublas":
@@ -315,7 +330,7 @@ class DecodeEngine:
                     n += 2
                 lo, hi = (0, cfg.ffn_dim) if self.tp is None else self.tp.ffn_range
                 _lib.check(L.ps_select_union(_lib.ptr(self.r_logits), B, cfg.ffn_dim, cfg.ffn_dim,
-                                             self.k_mlp[ell], 0.0, _lib.ptr(self.bitmap), _lib.ptr(self.ticket),
+                                             self.k_mlp[ell], 0.0, _lib.ptr(self.su_ws), self.su_bytes,
                                              lo, hi, ROW_PAD, _lib.ptr(self.union_idx),
                                              _lib.ptr(self.union_count), st), "ps_select_union")
                 n += 1
@@ -338,7 +353,7 @@ class DecodeEngine:
                     _lib.call("ps_swiglu", _lib.ptr(self.gu), self.gu.stride(0), B, mk.D, _lib.ptr(self.hidden),
                               self.hidden.stride(0), st)
                     n += 1
-                    self._dense_down(mk, self.hidden[:, :mk.D])
+                    pending = self._dense_down(mk, self.hidden[:, :mk.D])
                 else:
                     swiglu_into(mk, self.h, self.gu, self.hidden, self.x, residual=self.x)
                     n += 3
@@ -347,25 +362,21 @@ class DecodeEngine:
                 if self.dense_backend == "cublas":
                     hid = self._scratch("hid", (B, mk.D), torch.bfloat16)
                     n += self._linear_bf16(self.h, mk.w1t, mk.b1, hid, act_relu=True)
-                    self._dense_down(mk, hid)
+                    pending = self._dense_down(mk, hid)
                 else:
                     mlp_into(mk, self.h, None, None, self.hidden, self.x, residual=self.x)
                     n += 2
-        _lib.check(L.ps_layernorm(_lib.ptr(self.x), d, _lib.ptr(m.lnf_g), _lib.ptr(m.lnf_b), B, d,
-                                  _lib.ptr(self.h), d, st), "ps_layernorm")
-        n += 1
+        n += self._ln(m.lnf_g, m.lnf_b, pending)
         n += self._linear_f32(self.h, m.unembed_t, None, self.logits, tag="gg_lm")
         torch.argmax(self.logits, dim=1, out=self.next_tokens)
         return n
 
-    def _dense_down(self, mk, hid) -> None:
-        """x += hid @ W2 + b2 with W2^T stored neuron-major (D, d): a plain
-        (B, D) x (D, d) cuBLAS GEMM on the packed rows."""
-        tmp = self._scratch("down", self.x.shape, torch.float32)
-        torch.mm(hid, mk.w2t, out_dtype=torch.float32, out=tmp)
-        self.x.add_(tmp)
-        if mk.b2 is not None:
-            self.x.add_(mk.b2)
+    def _dense_down(self, mk, hid):
+        """x += hid @ W2 with W2^T stored neuron-major (D, d): a plain
+        (B, D) x (D, d) cuBLAS GEMM on the packed rows accumulating into x
+        (beta = 1).  Returns b2 as the pending bias of the next LN."""
+        torch.addmm(self.x, hid, mk.w2t, out_dtype=torch.float32, out=self.x)
+        return mk.b2
 
     def sel_bufs(self, k: int) -> torch.Tensor:
         key = f"_sel_{k}"

@@ -200,12 +200,12 @@ def union_from_logits(logits: torch.Tensor, k: int | None = None, threshold: flo
     dev = logits.device
     if k is not None and not 1 <= k <= width:
         raise ValueError(f"k must be in [1, {width}], got {k}")
-    bitmap = _ws.get("union_bitmap", ((width + 31) // 32) * 4, dev)
-    ticket = _ws.get("union_ticket", 4, dev)
+    nbytes = int(_lib.load().ps_select_union_workspace_bytes(rows, width))
+    ws = _ws.get(f"select_union_{rows}_{width}", nbytes, dev)
     buf = torch.empty(_round_up(width, ROW_PAD), dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.call("ps_select_union", _lib.ptr(logits), rows, width, width, int(k) if k is not None else 0,
-              float(threshold or 0.0), _lib.ptr(bitmap), _lib.ptr(ticket), 0, width, ROW_PAD, _lib.ptr(buf),
+              float(threshold or 0.0), _lib.ptr(ws), nbytes, 0, width, ROW_PAD, _lib.ptr(buf),
               _lib.ptr(cnt), _lib.stream_ptr())
     return NeuronIndexTensor(layer, buf, cnt)
 

@@ -64,6 +64,54 @@ def test_topk_random_large_vs_oracle():
         assert np.array_equal(got, po.topk_indices_rows(s, k))
 
 
+@pytest.mark.parametrize("dist", ["normal", "ties_few", "ties_many", "one_bin", "nan_inf", "wide"])
+def test_topk_and_union_paths_vs_oracle(dist):
+    """Every branch of the radix select: no ties (local decision), a few
+    ties at the k-th key (resolved among the threshold-bin candidates),
+    many ties / one crowded bin (full-row fallback), NaN and +-inf, rows
+    wider than the shared-memory staging limit."""
+    rng = np.random.default_rng(7)
+    rows, cols = 24, 16384
+    s = rng.normal(size=(rows, cols)).astype(np.float32)
+    if dist == "ties_few":
+        s = np.round(s * 1024) / 1024
+    elif dist == "ties_many":
+        s = np.round(s * 4) / 4
+    elif dist == "one_bin":
+        s = (1.0 + rng.random((rows, cols)) * 1e-4).astype(np.float32)
+    elif dist == "nan_inf":
+        s[:, ::97] = np.nan
+        s[:, 5::89] = np.inf
+        s[:, 7::83] = -np.inf
+        s[:, 11::79] = -0.0
+    elif dist == "wide":
+        rows, cols = 6, 50000
+        s = np.round(rng.normal(size=(rows, cols)).astype(np.float32) * 256) / 256
+    s = s.astype(np.float32)
+    for k in (1, 37, cols // 10, cols // 2, cols - 3):
+        got = pb.topk_indices_rows(t(s), k).cpu().numpy()
+        ref = po.topk_indices_rows(s, k)
+        assert np.array_equal(got, ref), (dist, k)
+        u = pb.union_from_logits(t(s), k=k)
+        assert np.array_equal(u.indices.cpu().numpy(), po.union_neuron_indices(list(ref))), (dist, k)
+
+
+@pytest.mark.parametrize("rows", [1, 64, 150, 300])
+def test_topk_union_cluster_shapes(rows):
+    """Row counts that pick every cluster split (8 / 4 / 2 / 1 CTAs per row)
+    with hot-neuron logits like the bench's router (a shared +20 bias)."""
+    rng = np.random.default_rng(rows)
+    cols = 16384
+    s = rng.normal(size=(rows, cols)).astype(np.float32)
+    s[:, rng.choice(cols, cols // 2, replace=False)] += 20.0
+    for k in (cols // 2, cols // 10):
+        ref = po.topk_indices_rows(s, k)
+        u = pb.union_from_logits(t(s), k=k)
+        assert np.array_equal(u.indices.cpu().numpy(), po.union_neuron_indices(list(ref))), k
+    got = pb.topk_indices_rows(t(s), cols // 10).cpu().numpy()
+    assert np.array_equal(got, po.topk_indices_rows(s, cols // 10))
+
+
 def test_union_bit_exact(golden):
     for i in range(int(golden["union_n"])):
         rows = golden[f"union_rows_{i}"]

@@ -118,16 +118,14 @@ def main():
             rep(f"sha_decode k={kh}/{H} ctx={ctx}", timeit(f, a.iters), nb)
     if not a.only or "sel" in a.only:
         logits = torch.randn(B, D, device=dev)
-        bm = torch.zeros((D + 31) // 32, dtype=torch.int32, device=dev)
+        nb = int(_lib.load().ps_select_union_workspace_bytes(B, D))
+        ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
         buf = torch.empty(D, dtype=torch.int32, device=dev)
         cnt = torch.zeros(1, dtype=torch.int32, device=dev)
         st = lambda: _lib.stream_ptr()  # noqa
-        tk = torch.zeros(1, dtype=torch.int32, device=dev)
-        f = lambda i: _lib.call("ps_select_union", logits.data_ptr(), B, D, D, int(a.union * D), 0.0, bm.data_ptr(),  # noqa
-                                tk.data_ptr(), 0, D, 128, buf.data_ptr(), cnt.data_ptr(), st())
+        f = lambda i: _lib.call("ps_select_union", logits.data_ptr(), B, D, D, int(a.union * D), 0.0, ws.data_ptr(),  # noqa
+                                nb, 0, D, 128, buf.data_ptr(), cnt.data_ptr(), st())
         rep(f"select_union (topk+union+compact) {B}x{D} k={int(a.union * D)}", timeit(f, a.iters), B * D * 4)
-        g = lambda i: _lib.call("ps_topk_rows", logits.data_ptr(), B, D, D, int(a.union * D), buf.data_ptr(), None, st())  # noqa
-        rep("topk_rows (ids only, k=D/2 would overflow buf; ids) ", timeit(lambda i: None, 1), 1)
         hr = pb.HeadRouter(d, 32, seed=1)
         sel = torch.empty(B, 16, dtype=torch.int32, device=dev)
         h = lambda i: hr.select_into(x, 16, sel)  # noqa

@@ -1,0 +1,44 @@
+"""Phase timeline of the top-k kernel (ps_debug_topk_trace)."""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2505_14884_b200 import _lib  # noqa: E402
+
+dev = torch.device("cuda")
+L = _lib.load()
+names = ["start", "staged", "bracket", "counted", "kth", "selected", "union", "-", "-", "-"]
+for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"), (256, 16384, 8192, "hot")]:
+    g = torch.Generator(device=dev); g.manual_seed(0)
+    lg = torch.randn(rows, cols, device=dev, generator=g)
+    if dist == "hot":
+        lg[:, torch.randperm(cols, device=dev, generator=g)[: cols // 2]] += 20.0
+    bm = torch.zeros((cols + 31) // 32, dtype=torch.int32, device=dev)
+    nb = int(_lib.load().ps_select_union_workspace_bytes(rows, cols))
+    ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
+    buf = torch.empty(cols, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    tk = torch.zeros(1, dtype=torch.int32, device=dev)
+    tr = torch.zeros(rows * 8 * 16, dtype=torch.int64, device=dev)
+    f = lambda: _lib.call("ps_select_union", lg.data_ptr(), rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
+                          nb, 0, cols, 128, buf.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    L.ps_debug_topk_trace(tr.data_ptr())
+    f()
+    torch.cuda.synchronize()
+    L.ps_debug_topk_trace(None)
+    t = tr.view(-1, 16).cpu().numpy()
+    t = t[t[:, 0] > 0]
+    t0 = t[:, 0].min()
+    print(f"== {rows}x{cols} k={k} {dist}: CTAs={len(t)}  span={(t[:, 5].max() - t0) / 1e3:.1f} us  "
+          f"fallbacks={int((t[:, 11] == 1).sum())}  cand(med)={int(np.median(t[:, 10] >> 32))} "
+          f"eq(max)={int((t[:, 10] & 0xffffffff).max())}")
+    for j in range(1, 10):
+        v = t[:, j]
+        ok = v > 0
+        if ok.any():
+            d = (v[ok] - t0) / 1e3
+            print(f"   {names[j]:9s} min {d.min():7.2f}  med {np.median(d):7.2f}  max {d.max():7.2f} us")
+    print(f"   start     min {0:7.2f}  med {np.median((t[:, 0] - t0) / 1e3):7.2f}  max {(t[:, 0].max() - t0) / 1e3:7.2f}")
