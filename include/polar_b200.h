@@ -46,6 +46,8 @@ extern "C" {
 #define PS_ACT_RELU 1
 
 int ps_version(void);
+/* programmatic dependent launch of every kernel (default on); 0 disables */
+void ps_set_pdl(int enable);
 const char* ps_status_string(int status);
 /* number of SMs of the current device (grid sizing helper) */
 int ps_num_sms(void);
@@ -117,10 +119,12 @@ int ps_threshold_rows(const float* logits, int rows, int cols, int64_t ld, float
  * words are stored into the workspace, the last CTA of every 16-row group
  * ORs the group, and the last group compacts bits [lo, hi) into union_out /
  * count_out exactly as ps_bitmap_compact does.  No contended atomics.
+ * bias: f32 (cols) added to every row before selection (the router's output
+ * bias, routers.py:286-288), or NULL.  rows <= 1024.
  * ws >= ps_select_union_workspace_bytes(rows, cols), zero-filled before its
  * first use (its tickets self-reset; the bitmaps are fully rewritten). */
 size_t ps_select_union_workspace_bytes(int rows, int cols);
-int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr,
+int ps_select_union(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k, float thr,
                     void* ws, size_t ws_bytes, int lo, int hi, int pad,
                     int32_t* union_out, int32_t* count_out, void* stream);
 /* debug: per-CTA phase timestamps of the top-k kernel (16 x u64 per CTA), NULL = off */
@@ -175,17 +179,23 @@ void ps_debug_gemm_trace(void* buf, int stages, int target_ctas);
 /* A-operand copy engine: 0 = TMA (tile / tile::gather4), 1 = cp.async loader
  * warps for gathered rows (default), 2 = cp.async loader warps always */
 void ps_debug_gemm_lsu_mode(int mode);
+/* flags: PS_GG_A_READY -- w_rows, idx and count_dev were written at least
+ * two launches earlier in the stream (or are static): the A stream may start
+ * before the immediately preceding kernel completes (programmatic dependent
+ * launch).  Without it (or with idx == count_dev == NULL, i.e. static dense
+ * weights, where it is implied) only static data is read early. */
+#define PS_GG_A_READY 1
 size_t ps_gather_gemm_workspace_bytes(int N, int M, int K, int splits);
 int ps_gather_gemm_auto_splits(int N, int M, int K);
 int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                    const void* x, int64_t x_ld, const float* bias,
                    const float* residual, int64_t residual_ld,
-                   int N, int M, int K, int act, int splits,
+                   int N, int M, int K, int act, int splits, int flags,
                    void* out, int64_t out_ld, int out_dtype,
                    void* ws, size_t ws_bytes, void* stream);
 int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                      const void* h, int64_t h_ld, const float* bias, const float* residual,
-                     int64_t residual_ld, int N, int M, int K_max, int splits,
+                     int64_t residual_ld, int N, int M, int K_max, int splits, int flags,
                      void* out, int64_t out_ld, int out_dtype,
                      void* ws, size_t ws_bytes, void* stream);
 

@@ -19,6 +19,7 @@ PS_DTYPE_F32 = 0
 PS_DTYPE_BF16 = 1
 PS_ACT_NONE = 0
 PS_ACT_RELU = 1
+PS_GG_A_READY = 1
 
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
@@ -39,7 +40,7 @@ SIGNATURES = {
     "ps_topk_rows": (_i, [_vp, _i, _i, _i64, _i, _vp, _vp, _vp]),
     "ps_threshold_rows": (_i, [_vp, _i, _i, _i64, _f, _vp, _vp]),
     "ps_select_union_workspace_bytes": (_sz, [_i, _i]),
-    "ps_select_union": (_i, [_vp, _i, _i, _i64, _i, _f, _vp, _sz, _i, _i, _i, _vp, _vp, _vp]),
+    "ps_select_union": (_i, [_vp, _vp, _i, _i, _i64, _i, _f, _vp, _sz, _i, _i, _i, _vp, _vp, _vp]),
     "ps_union_rows": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ps_bitmap_compact": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_head_router_topk": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp]),
@@ -48,10 +49,11 @@ SIGNATURES = {
     "ps_debug_topk_trace": (None, [_vp]),
     "ps_gather_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "ps_gather_gemm_auto_splits": (_i, [_i, _i, _i]),
-    "ps_gather_gemm": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i,
+    "ps_gather_gemm": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i, _i,
                             _vp, _i64, _i, _vp, _sz, _vp]),
-    "ps_gather_gemm_t": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i,
+    "ps_gather_gemm_t": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i,
                               _vp, _i64, _i, _vp, _sz, _vp]),
+    "ps_set_pdl": (None, [_i]),
     "ps_layernorm": (_i, [_vp, _i64, _vp, _vp, _i, _i, _vp, _i64, _vp]),
     "ps_add_layernorm": (_i, [_vp, _i64, _vp, _vp, _vp, _i, _i, _vp, _i64, _vp]),
     "ps_embed": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp]),

@@ -31,6 +31,45 @@ inline int launch_status() {
   return e == cudaSuccess ? PS_OK : PS_ERR_CUDA;
 }
 
+// ---------------------------------------------------------------- launches
+// Programmatic dependent launch (PDL): every libpolar kernel is launched with
+// programmatic stream serialization, so its CTAs may start while the
+// previous kernel in the stream drains.  Each kernel runs its input-
+// independent prologue (barrier init, TMEM alloc, tensor-map prefetch,
+// reads of data produced >= 2 kernels earlier), then griddep_wait() before
+// touching the predecessor's output, then griddep_launch() to let its own
+// successor start early.  Every kernel waits before it exits, so completion
+// stays transitive along the stream.  g_pdl = 0 (ps_set_pdl) disables it.
+extern int g_pdl;
+
+template <typename... KArgs, typename... Args>
+inline int launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (g_pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) != cudaSuccess) return PS_ERR_CUDA;
+  return launch_status();
+}
+
 // ---------------------------------------------------------------- bf16
 PS_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 PS_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
@@ -242,6 +281,13 @@ PS_DEV void red_add_v4(float* addr, float4 v) {
                "f"(v.w)
                : "memory");
 }
+
+// ---------------------------------------------------------------- PDL (device side)
+// wait until the previous grid in the stream has completed and its writes
+// are visible (no-op without a programmatic dependency)
+PS_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the next grid in the stream to start launching
+PS_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------- clusters / DSMEM
 PS_DEV uint32_t cluster_rank() {

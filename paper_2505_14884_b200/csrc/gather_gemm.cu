@@ -29,6 +29,7 @@
 //     accumulator (tcgen05.ld 32x32b) through a shared-memory staging tile and
 //     apply bias / ReLU / residual with 16-byte vector stores.
 #include <cuda.h>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -67,6 +68,7 @@ struct GGParams {
   int64_t out_ld;
   int out_bf16;
   int vec_ok;  // out / residual rows 16-byte aligned: vector epilogue stores
+  int a_early;  // A (weights, idx, count) ready before the previous kernel ends: stream A pre-griddep_wait
   unsigned long long* trace;  // debug: per-CTA timestamps (ps_debug_gemm_trace), NULL normally
 };
 
@@ -92,6 +94,11 @@ PS_DEV uint32_t num_clusters() {
 }
 PS_DEV void remote_arrive(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+// relaxed remote arrive: no fence (MEMBAR.GPU) -- for "done reading your
+// staging tile" signals whose loads already returned their data
+PS_DEV void remote_arrive_relaxed(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 PS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
@@ -149,6 +156,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     tr[7] = smid;
   }
 
+  // ---- PDL: with the A operand ready (static weights, or ids produced >= 2
+  // launches earlier) only the B / epilogue roles wait for the previous grid
+  if (!p.a_early) {
+    griddep_wait();
+    if (tid == 0) griddep_launch();
+  }
   // ---- device-side work partition (identical in every role and CTA of a cluster)
   const int count = p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K);
   const int klimit = (MODE == MODE_UP) ? p.K : count;
@@ -160,7 +173,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int nkb = max(0, min(kbt, kb0 + per) - kb0);  // K blocks of this CTA (same for every tile)
   const int my_tiles = cid < tiles ? (tiles - cid + ncl - 1) / ncl : 0;
   // every CTA of a cluster sees the same my_tiles, so whole clusters leave together
-  if (my_tiles == 0) return;
+  if (my_tiles == 0) {
+    if (p.a_early) {
+      griddep_wait();
+      if (tid == 0) griddep_launch();
+    }
+    return;
+  }
 
   const uint32_t tcols = NB <= 16 ? 32 : (NB <= 32 ? 64 : (NB <= 64 ? 128 : (NB <= 128 ? 256 : 512)));
   if (warp == kMmaWarp) {
@@ -186,9 +205,11 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_before();
   __syncthreads();
   // peers' barriers must be initialised before any remote arrive
+  // (fence_mbar_init already released the inits at cluster scope: a relaxed
+  //  barrier suffices and avoids a MEMBAR.GPU)
   if (C > 1) {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -205,6 +226,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int j = 0; j < 4; ++j) r[j] = base + j < lim ? __ldg(p.idx + base + j) : first;
       return make_int4(r[0], r[1], r[2], r[3]);
     };
+    if (p.a_early) {
+      griddep_wait();
+      if (lane == 0) griddep_launch();
+    }
     int i = 0;
     for (int j = 0; j < my_tiles; ++j) {
       const int t = tile_of(j);
@@ -349,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
+    if (p.a_early) griddep_wait();       // residual / out belong to the previous grid's stream order
     const int q = warp & 3;               // TMEM lane quadrant of this warp
     const int m = q * 32 + lane;          // tile row (TMEM lane)
     const int et = tid - kEpiWarp0 * 32;  // 0..127
@@ -383,21 +409,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (my_live[u] && p.bias)
           my_bias[u] = __ldg(p.bias + ((MODE == MODE_UP && p.idx) ? __ldg(p.idx + gm) : gm));
       }
-      auto finish4 = [&](int n, float4 v) {
-        const int gm0 = m0 + my_m;
-        const size_t o = (size_t)(n0 + n) * p.out_ld + gm0;
-        float vv[4] = {v.x, v.y, v.z, v.w};
+      auto load_res = [&](int n) -> float4 {
         float res[4] = {0.f, 0.f, 0.f, 0.f};
+        const int gm0 = m0 + my_m;
         if (p.residual) {
           if (p.vec_ok && gm0 + 4 <= p.M) {
-            const float4 r4 = *reinterpret_cast<const float4*>(p.residual + (size_t)(n0 + n) * p.res_ld + gm0);
-            res[0] = r4.x; res[1] = r4.y; res[2] = r4.z; res[3] = r4.w;
+            return *reinterpret_cast<const float4*>(p.residual + (size_t)(n0 + n) * p.res_ld + gm0);
           } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
               if (gm0 + u < p.M) res[u] = p.residual[(size_t)(n0 + n) * p.res_ld + gm0 + u];
           }
         }
+        return make_float4(res[0], res[1], res[2], res[3]);
+      };
+      auto finish4r = [&](int n, float4 v, float4 r4) {
+        const int gm0 = m0 + my_m;
+        const size_t o = (size_t)(n0 + n) * p.out_ld + gm0;
+        float vv[4] = {v.x, v.y, v.z, v.w};
+        float res[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           float x = 0.f;
@@ -428,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
         }
       };
+      auto finish4 = [&](int n, float4 v) { finish4r(n, v, load_res(n)); };
 
       mbar_wait(&tfull[a], (j >> 1) & 1);
       if (tr && et == 0 && j == 0) tr[8] = gtimer();
@@ -453,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (lane == 0) mbar_arrive(&tempty[a]);  // accumulator free for the MMA warp
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
+        if (tr && et == 0 && j == 0 && cb == 0) tr[10] = gtimer();
         const int rows_here = min(ncb, nrows - cb);
         if (C == 1) {
           for (int v = et; v < rows_here * vec_per_n; v += kEpiThreads) {
@@ -461,30 +493,56 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
         } else {
-          // 2) every CTA staged: reduce my rows over the C partials in rank order
+          // 2) every CTA staged: reduce my rows over the C partials in rank
+          //    order.  A thread owns <= kVecT vectors (C >= 2); its residual
+          //    rows are fetched before the wait and all C x kVecT DSMEM loads
+          //    are issued before the first use.
+          constexpr int kVecT = (kEpiCols * BM / 8) / kEpiThreads;  // 8
+          const int nvec = rows_here * vec_per_n;
           if (et == 0)
             for (int c = 0; c < C; ++c) remote_arrive(peer_rdy[c]);
           mbar_wait_cluster(rdy, use & 1);
-          for (int v = et; v < rows_here * vec_per_n; v += kEpiThreads) {
-            const int n = v / vec_per_n;
-            const uint32_t off = (uint32_t)((n * BM + my_m) * 4);
-            float4 acc[kMaxCluster];
+          if (tr && et == 0 && j == 0 && cb == 0) tr[11] = gtimer();
+          auto reduce = [&](auto cc) {
+            constexpr int CC = decltype(cc)::value;
+            constexpr int NV = 2 * kVecT / CC;  // vectors per thread at this cluster size
+            constexpr int GV = 8 / CC;          // vectors per load batch (8 DSMEM float4 in flight)
 #pragma unroll
-            for (int c = 0; c < kMaxCluster; ++c)
-              if (c < C) acc[c] = ld_dsmem_v4(peer_stg[c] + off);
-            float4 sum = acc[0];
+            for (int g0 = 0; g0 < NV; g0 += GV) {
+              float4 buf[GV][CC], res[GV];
 #pragma unroll
-            for (int c = 1; c < kMaxCluster; ++c)
-              if (c < C) {
-                sum.x += acc[c].x; sum.y += acc[c].y; sum.z += acc[c].z; sum.w += acc[c].w;
+              for (int gi = 0; gi < GV; ++gi) {
+                const int v = et + (g0 + gi) * kEpiThreads;
+                const uint32_t off = (uint32_t)(((v / vec_per_n) * BM + my_m) * 4);
+                res[gi] = v < nvec ? load_res(cb + v / vec_per_n) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < CC; ++c)
+                  buf[gi][c] = v < nvec ? ld_dsmem_v4(map_peer(stg_s, c) + off) : make_float4(0.f, 0.f, 0.f, 0.f);
               }
-            finish4(cb + n, sum);
-          }
+#pragma unroll
+              for (int gi = 0; gi < GV; ++gi) {
+                const int v = et + (g0 + gi) * kEpiThreads;
+                if (v < nvec) {
+                  float4 sum = buf[gi][0];
+#pragma unroll
+                  for (int c = 1; c < CC; ++c) {
+                    sum.x += buf[gi][c].x; sum.y += buf[gi][c].y; sum.z += buf[gi][c].z; sum.w += buf[gi][c].w;
+                  }
+                  finish4r(cb + v / vec_per_n, sum, res[gi]);
+                }
+              }
+            }
+          };
+          if (C == 2) reduce(std::integral_constant<int, 2>{});
+          else if (C == 4) reduce(std::integral_constant<int, 4>{});
+          else reduce(std::integral_constant<int, 8>{});
           // 3) done reading the peers' staging tiles
           asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));
           if (et == 0)
-            for (int c = 0; c < C; ++c) remote_arrive(peer_fre[c]);
+            for (int c = 0; c < C; ++c) remote_arrive_relaxed(peer_fre[c]);
+          if (tr && et == 0 && j == 0 && cb == 0) tr[12] = gtimer();
           mbar_wait_cluster(fre, use & 1);
+          if (tr && et == 0 && j == 0 && cb == 0) tr[13] = gtimer();
           ++use;
         }
       }
@@ -563,7 +621,8 @@ int make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uin
 }
 
 template <int MODE, bool GATHER, bool LSU_A>
-int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GGParams& prm, int cluster, cudaStream_t st) {
+int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GGParams& prm, int cluster, int work_ctas,
+             cudaStream_t st) {
   const size_t smem = smem_bytes(prm.NB, prm.stages);
   auto kern = gather_gemm_kernel<MODE, GATHER, LSU_A>;
   static bool configured = false;
@@ -574,21 +633,12 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GGParams& prm, 
       return PS_ERR_CUDA;
     configured = true;
   }
-  const int grid = (cta_slots(prm.NB) / cluster) * cluster;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, prm) != cudaSuccess) return PS_ERR_CUDA;
-  return launch_status();
+  // persistent grid: the CTA slots, but no more than the expected work (idle
+  // CTAs would only occupy slots the next kernel's early (PDL) CTAs can use);
+  // more live tiles than expected are picked up by the tile loop
+  int grid = (cta_slots(prm.NB) / cluster) * cluster;
+  if (work_ctas > 0 && work_ctas < grid) grid = work_ctas;
+  return launch_ex(kern, dim3(grid), dim3(kThreads), smem, st, cluster, ta, tb, prm);
 }
 
 // w_rows: (w_rows_n, w_cols) row-major; B operand x: (N, kx) with row stride x_ld
@@ -605,12 +655,13 @@ int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, int tile
     rc = make_map(&ta, prm.w, (uint64_t)w_cols, (uint64_t)w_rows_n, (uint64_t)prm.w_ld, 64, gather ? 1 : BK);
   if (rc != PS_OK) return rc;
   const int cluster = pick_cluster(prm.NB, tiles_est * prm.n_tiles, kbt_est);
+  const int work = tiles_est * prm.n_tiles * cluster;
   const bool lsu = g_lsu_mode == 2 || (g_lsu_mode == 1 && gather);
   if (gather)
-    return lsu ? launch_t<MODE, true, true>(ta, tb, prm, cluster, st)
-               : launch_t<MODE, true, false>(ta, tb, prm, cluster, st);
-  return lsu ? launch_t<MODE, false, true>(ta, tb, prm, cluster, st)
-             : launch_t<MODE, false, false>(ta, tb, prm, cluster, st);
+    return lsu ? launch_t<MODE, true, true>(ta, tb, prm, cluster, work, st)
+               : launch_t<MODE, true, false>(ta, tb, prm, cluster, work, st);
+  return lsu ? launch_t<MODE, false, true>(ta, tb, prm, cluster, work, st)
+             : launch_t<MODE, false, false>(ta, tb, prm, cluster, work, st);
 }
 
 }  // namespace
@@ -656,14 +707,15 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
   prm.out = out;
   prm.out_ld = out_ld;
   prm.out_bf16 = out_dtype == PS_DTYPE_BF16;
+  prm.a_early = 0;
   prm.vec_ok = (out_ld % 4 == 0) && ((uintptr_t)out % 16 == 0);
   return PS_OK;
 }
 
 extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                               const void* x, int64_t x_ld, const float* bias, const float* residual,
-                              int64_t residual_ld, int N, int M, int K, int act, int splits, void* out, int64_t out_ld,
-                              int out_dtype, void* ws, size_t ws_bytes, void* stream) {
+                              int64_t residual_ld, int N, int M, int K, int act, int splits, int flags, void* out,
+                              int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
   (void)ws; (void)ws_bytes;
   if (K % 8 || x_ld < K || out_ld < M) return PS_ERR_VALUE;
   GGParams prm;
@@ -671,6 +723,7 @@ extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* i
   if (st != PS_OK) return st;
   prm.w_ld = K;
   prm.act = act;
+  prm.a_early = (!idx && !count_dev) || (flags & PS_GG_A_READY);
   prm.residual = residual;
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;
@@ -682,14 +735,15 @@ extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* i
 
 extern "C" int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                                 const void* h, int64_t h_ld, const float* bias, const float* residual,
-                                int64_t residual_ld, int N, int M, int K_max, int splits, void* out, int64_t out_ld,
-                                int out_dtype, void* ws, size_t ws_bytes, void* stream) {
+                                int64_t residual_ld, int N, int M, int K_max, int splits, int flags, void* out,
+                                int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
   (void)ws; (void)ws_bytes;
   if (M % 8 || h_ld < K_max || out_ld < M) return PS_ERR_VALUE;
   GGParams prm;
   int st = gg_common(prm, w_rows, idx, count_dev, h, h_ld, bias, N, M, K_max, out, out_ld, out_dtype);
   if (st != PS_OK) return st;
   prm.w_ld = M;
+  prm.a_early = (!idx && !count_dev) || (flags & PS_GG_A_READY);
   prm.residual = residual;
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;

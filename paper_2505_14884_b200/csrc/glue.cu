@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(kKvThreads) kv_append_kernel(uint16_t* __restr
                                                                const uint16_t* __restrict__ vn, int64_t src_ld,
                                                                int H_kv, int cap, int d_h, int32_t* err_flag) {
   const int b = blockIdx.x;
+  griddep_wait();
+  griddep_launch();
   const int pos = lengths[b];
   if (pos >= cap) {
     if (threadIdx.x == 0 && err_flag) *err_flag = 1;
@@ -69,6 +71,8 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(float* __restrict
                                                                uint16_t* __restrict__ y, int64_t y_ld) {
   __shared__ float red[2][kLnThreads / 32];
   float* xr = x + (size_t)blockIdx.x * x_ld;
+  griddep_wait();
+  griddep_launch();
   const int n4 = d >> 2;
   float4 v[kLnSlots];
   float s = 0.f;
@@ -128,6 +132,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __r
                              const uint16_t* __restrict__ emb, const uint16_t* __restrict__ pos, int d,
                              float* __restrict__ x) {
   const int b = blockIdx.x;
+  griddep_wait();
+  griddep_launch();
   const uint16_t* er = emb + (size_t)tok[b] * d;
   const uint16_t* pr = pos + (size_t)len[b] * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x)
@@ -137,6 +143,8 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __r
 // h = silu(gate) * up, gate/up from one (B, 2D) bf16 row [gate | up]
 __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int64_t gu_ld, int B, int D,
                               uint16_t* __restrict__ h, int64_t h_ld) {
+  griddep_wait();
+  griddep_launch();
   const int64_t total = (int64_t)B * D;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(e / D), j = (int)(e - (int64_t)b * D);
@@ -149,12 +157,15 @@ __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int64_t gu_ld, in
 }  // namespace
 
 int g_num_sms = 0;
+int g_pdl = 1;
 
 }  // namespace ps
 
 using namespace ps;
 
 extern "C" int ps_version(void) { return 1; }
+
+extern "C" void ps_set_pdl(int enable) { g_pdl = enable ? 1 : 0; }
 
 extern "C" const char* ps_status_string(int status) {
   switch (status) {
@@ -188,10 +199,10 @@ extern "C" int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths, cons
   if (!k_cache || !v_cache || !lengths || !k_new || !v_new) return PS_ERR_VALUE;
   if (((uintptr_t)k_new % 16) || ((uintptr_t)v_new % 16) || ((uintptr_t)k_cache % 16) || ((uintptr_t)v_cache % 16))
     return PS_ERR_VALUE;
-  kv_append_kernel<<<B, kKvThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths, static_cast<const uint16_t*>(k_new),
-      static_cast<const uint16_t*>(v_new), src_ld, H_kv, cap, d_h, err_flag);
-  return launch_status();
+  return launch_ex(kv_append_kernel, dim3(B), dim3(kKvThreads), 0, static_cast<cudaStream_t>(stream), 1,
+                   static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths,
+                   static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), src_ld, H_kv, cap, d_h,
+                   err_flag);
 }
 
 static int ln_launch(float* x, int64_t x_ld, const float* add, const float* gamma, const float* beta, int B, int d,
@@ -203,12 +214,8 @@ static int ln_launch(float* x, int64_t x_ld, const float* add, const float* gamm
       (add && ((uintptr_t)add % 16)))
     return PS_ERR_VALUE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (add)
-    layernorm_kernel<true><<<B, kLnThreads, 0, st>>>(x, x_ld, add, gamma, beta, d, static_cast<uint16_t*>(y), y_ld);
-  else
-    layernorm_kernel<false><<<B, kLnThreads, 0, st>>>(x, x_ld, nullptr, gamma, beta, d, static_cast<uint16_t*>(y),
-                                                      y_ld);
-  return launch_status();
+  return launch_ex(add ? layernorm_kernel<true> : layernorm_kernel<false>, dim3(B), dim3(kLnThreads), 0, st, 1, x,
+                   x_ld, add, gamma, beta, d, static_cast<uint16_t*>(y), y_ld);
 }
 
 extern "C" int ps_layernorm(const float* x, int64_t x_ld, const float* gamma, const float* beta, int B, int d,
@@ -224,10 +231,8 @@ extern "C" int ps_add_layernorm(float* x, int64_t x_ld, const float* add, const 
 extern "C" int ps_embed(const int32_t* tokens, const int32_t* lengths, const void* embed, const void* pos_embed,
                         int B, int d, float* x, void* stream) {
   if (B < 1 || d < 1 || !tokens || !lengths || !embed || !pos_embed || !x) return PS_ERR_VALUE;
-  embed_kernel<<<B, 256, 0, static_cast<cudaStream_t>(stream)>>>(tokens, lengths,
-                                                                 static_cast<const uint16_t*>(embed),
-                                                                 static_cast<const uint16_t*>(pos_embed), d, x);
-  return launch_status();
+  return launch_ex(embed_kernel, dim3(B), dim3(256), 0, static_cast<cudaStream_t>(stream), 1, tokens, lengths,
+                   static_cast<const uint16_t*>(embed), static_cast<const uint16_t*>(pos_embed), d, x);
 }
 
 extern "C" int ps_swiglu(const void* gu, int64_t gu_ld, int B, int D, void* h, int64_t h_ld, void* stream) {
@@ -235,7 +240,6 @@ extern "C" int ps_swiglu(const void* gu, int64_t gu_ld, int B, int D, void* h, i
   const int64_t total = (int64_t)B * D;
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
-  swiglu_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint16_t*>(gu), gu_ld, B, D,
-                                                                     static_cast<uint16_t*>(h), h_ld);
-  return launch_status();
+  return launch_ex(swiglu_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 1,
+                   static_cast<const uint16_t*>(gu), gu_ld, B, D, static_cast<uint16_t*>(h), h_ld);
 }

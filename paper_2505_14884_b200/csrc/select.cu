@@ -51,6 +51,7 @@ constexpr int kTopkSmemCols = 40960;  // rows up to this width are staged in sha
 constexpr int kSample = 2048;         // strided sample of a row that brackets the k-th key
 constexpr int kMaxCand = 3072;        // keys inside the bracket kept for the exact select
 constexpr int kGroupRows = 16;        // union: rows ORed by the last CTA of each row group
+constexpr int kMaxGroups = 64;        // ps_select_union: rows <= 1024
 
 struct TopkParams {
   const float* logits;
@@ -58,6 +59,7 @@ struct TopkParams {
   int64_t ld;
   int k;             // > 0: top-k per row; <= 0: threshold selection (logit > thr)
   float thr;
+  const float* bias;  // added to every row before selection (router output bias), or NULL
   int32_t* idx_out;  // (rows, k) ascending ids, or NULL
   uint32_t* bitmap;  // atomic-OR union bitmap, or NULL
   // fused union (ps_select_union): per-row words, per-group words, tickets
@@ -98,6 +100,34 @@ PS_DEV void select_bin(const int* g, int bins, int remaining, int* s_warp, int* 
         break;
       }
       cum += c;
+    }
+  }
+  __syncthreads();
+}
+
+// select_bin for two ranks in one scan: s_sel = {bin1, rem1, cnt1, bin2, rem2, cnt2}
+template <int NT>
+PS_DEV void select_bin2(const int* g, int bins, int r1, int r2, int* s_warp, int* s_sel) {
+  const int per = bins / NT;
+  const int hi = bins - (int)threadIdx.x * per;
+  int loc = 0;
+  for (int j = 1; j <= per; ++j) loc += g[hi - j];
+  const int above = block_excl_scan<NT>(loc, s_warp, nullptr);
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int r = t ? r2 : r1;
+    if (above < r && above + loc >= r) {
+      int cum = above;
+      for (int j = 1; j <= per; ++j) {
+        const int c = g[hi - j];
+        if (cum + c >= r) {
+          s_sel[3 * t] = hi - j;
+          s_sel[3 * t + 1] = r - cum;
+          s_sel[3 * t + 2] = c;
+          break;
+        }
+        cum += c;
+      }
     }
   }
   __syncthreads();
@@ -144,11 +174,16 @@ PS_DEV unsigned long long gtime() {
 #define TK_STAMP(slot) \
   do { if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 16 + (slot)] = gtime(); } while (0)
 
-// words [w0, w1) of the OR over `nrows` bitmaps (stride `words`), plain loads
+// word w of the OR over `nrows` (<= MAXR) bitmaps of stride `words`: every
+// load issued before the first use (one memory latency)
+template <int MAXR>
 PS_DEV uint32_t or_rows(const uint32_t* bits, int nrows, int words, int w) {
+  uint32_t v[MAXR];
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) v[r] = r < nrows ? __ldcg(bits + (size_t)r * words + w) : 0u;
   uint32_t acc = 0;
-#pragma unroll 4
-  for (int r = 0; r < nrows; ++r) acc |= __ldcg(bits + (size_t)r * words + w);
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) acc |= v[r];
   return acc;
 }
 
@@ -194,70 +229,98 @@ PS_DEV void compact_words(WordFn word, int lo, int hi, int pad, int32_t* out, in
 
 // Per-row top-k (and threshold selection), bit-exact with numpy's stable
 // argsort of -scores: value descending, ties -> lower index, -0.0 == +0.0,
-// NaN below -inf.  One CTA (1024 threads) per row; the row is staged in
-// shared memory as order-preserving u32 keys.
+// NaN below -inf.  One CTA (1024 threads) per row; the row (+ optional
+// bias) is staged in shared memory as order-preserving u32 keys.
 //   1. bracket: a strided sample of 2048 keys, taken while staging, gives
 //      the sample order statistics at ranks k*S/cols -/+ (3 sigma + 2) to
-//      22-bit precision (two shared radix passes);
+//      22-bit precision (two shared radix passes, both ranks per scan);
 //   2. one pass counts the keys above the bracket and appends the keys
-//      inside it (~7 % of the row) to a candidate list;
+//      inside it (~7 % of the row) to per-warp candidate lists (no shared
+//      atomics), then compacted;
 //   3. exact k-th key T = radix select over the candidates; ties at T go to
 //      the lowest columns: the last one taken, I, is a radix select over the
 //      tied candidates' inverted columns;
 //   4. every key is then decided locally (key > T, or key == T and column
 //      <= I): one ballot per 32 columns.
 // The bracket is verified exactly (count above < k <= above + candidates);
-// a miss falls back to a full 3-pass radix select with per-warp tie ranking.
-// Outputs: ids (ps_topk_rows), an atomic-OR bitmap, or -- ps_select_union --
-// this row's words stored plainly; the last CTA of each group of 16 rows ORs
-// the group, and the last group compacts the union (ascending ids, device
-// count, padded): no contended atomics.  Threshold mode keeps logit > thr.
+// a miss (or a per-warp list overflow) falls back to a full 3-pass radix
+// select with per-warp tie ranking.  Outputs: ids (ps_topk_rows), an
+// atomic-OR bitmap, or -- ps_select_union -- this row's words stored
+// plainly; the last CTA of each group of 16 rows ORs the group, and the last
+// group compacts the union (ascending ids, device count, padded): no
+// contended atomics.  Threshold mode keeps logit (+ bias) > thr.
+constexpr int kWarpCand = kMaxCand / kTopkWarps;  // per-warp candidate capacity
+constexpr int kStageVec = kTopkSmemCols / 4 / kTopkThreads;  // float4 per thread when staging
+
 __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   int* hist = reinterpret_cast<int*>(smem);                          // [4096]
   uint32_t* samp = reinterpret_cast<uint32_t*>(hist + 4096);         // [kMaxCand] samples, then tied cols
-  uint32_t* cand_key = samp + kMaxCand;                              // [kMaxCand]
+  uint32_t* wc_key = samp + kMaxCand;                                // [kMaxCand] per-warp lists
+  int* wc_idx = reinterpret_cast<int*>(wc_key + kMaxCand);           // [kMaxCand]
+  uint32_t* cand_key = reinterpret_cast<uint32_t*>(wc_idx + kMaxCand);  // [kMaxCand] compacted
   int* cand_idx = reinterpret_cast<int*>(cand_key + kMaxCand);       // [kMaxCand]
   uint32_t* keys = reinterpret_cast<uint32_t*>(cand_idx + kMaxCand);  // [cols] if staged
   __shared__ int s_warp[32];
-  __shared__ int s_eq[kTopkWarps], s_gt[kTopkWarps];
-  __shared__ int s_sel[3];
-  __shared__ int s_nc, s_na, s_n2, s_last;
+  __shared__ int s_eq[kTopkWarps], s_gt[kTopkWarps], s_wn[kTopkWarps];
+  __shared__ int s_sel[6];
+  __shared__ int s_na, s_ovf, s_n2, s_last;
   const int row = blockIdx.x, cols = p.cols;
   const float* x = p.logits + (size_t)row * p.ld;
+  const float* bias = p.bias;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool threshold = p.k <= 0;
   const bool staged = !threshold && cols <= kTopkSmemCols;
-  auto key_at = [&](int i) -> uint32_t { return staged ? keys[i] : order_key(__ldg(x + i)); };
-
+  auto logit = [&](int i) -> float { return bias ? __ldg(x + i) + __ldg(bias + i) : __ldg(x + i); };
+  auto key_at = [&](int i) -> uint32_t { return staged ? keys[i] : order_key(logit(i)); };
+  griddep_wait();
+  griddep_launch();
   TK_STAMP(0);
   uint32_t prefix = 0;
   int remaining = 0;
   bool fast = true;          // every key decided locally
   int tie_lim = 0x7fffffff;  // fast: tied keys at column < tie_lim are taken
   if (!threshold) {
-    if (tid == 0) { s_nc = 0; s_na = 0; s_n2 = 0; }
+    if (tid == 0) { s_na = 0; s_ovf = 0; s_n2 = 0; }
     for (int i = tid; i < 4096; i += kTopkThreads) hist[i] = 0;
-    // ---- stage the keys, keep a strided sample
+    // ---- stage the keys (all loads issued first), keep a strided sample
     const int S = min(cols, kSample);
     const int stride = cols / S;
-    if (staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0) {
+    if (staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0 &&
+        (!bias || ((uintptr_t)bias & 15) == 0)) {
       const float4* x4 = reinterpret_cast<const float4*>(x);
-      for (int i = tid; i < (cols >> 2); i += kTopkThreads) {
-        const float4 v = __ldg(x4 + i);
-        const uint4 u = make_uint4(order_key(v.x), order_key(v.y), order_key(v.z), order_key(v.w));
-        *reinterpret_cast<uint4*>(keys + 4 * i) = u;
-        const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+      const float4* b4 = reinterpret_cast<const float4*>(bias);
+      const int n4 = cols >> 2;
+      float4 v[kStageVec], bb[kStageVec];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int e = 4 * i + j;
-          if (e % stride == 0 && e / stride < S) samp[e / stride] = uu[j];
+      for (int j = 0; j < kStageVec; ++j) {
+        const int i = j * kTopkThreads + tid;
+        if (i < n4) {
+          v[j] = __ldg(x4 + i);
+          if (bias) bb[j] = __ldg(b4 + i);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kStageVec; ++j) {
+        const int i = j * kTopkThreads + tid;
+        if (i < n4) {
+          if (bias) {
+            v[j].x += bb[j].x; v[j].y += bb[j].y; v[j].z += bb[j].z; v[j].w += bb[j].w;
+          }
+          const uint4 u = make_uint4(order_key(v[j].x), order_key(v[j].y), order_key(v[j].z), order_key(v[j].w));
+          *reinterpret_cast<uint4*>(keys + 4 * i) = u;
+          const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int e = 4 * i + t;
+            if (e % stride == 0 && e / stride < S) samp[e / stride] = uu[t];
+          }
         }
       }
     } else {
       if (staged)
-        for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(__ldg(x + i));
-      for (int j = tid; j < S; j += kTopkThreads) samp[j] = order_key(__ldg(x + (size_t)j * stride));
+        for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(logit(i));
+      for (int j = tid; j < S; j += kTopkThreads) samp[j] = order_key(logit(j * stride));
     }
     __syncthreads();
     TK_STAMP(1);
@@ -274,10 +337,8 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       hist_add_agg(hist, j < S, u >> 20, lane);
     }
     __syncthreads();
-    select_bin<kTopkThreads>(hist, 4096, r_hi, s_warp, s_sel);
-    const int bin_hi = s_sel[0], rem_hi = s_sel[1];
-    select_bin<kTopkThreads>(hist, 4096, r_lo, s_warp, s_sel);
-    const int bin_lo = s_sel[0], rem_lo = s_sel[1];
+    select_bin2<kTopkThreads>(hist, 4096, r_hi, r_lo, s_warp, s_sel);
+    const int bin_hi = s_sel[0], rem_hi = s_sel[1], bin_lo = s_sel[3], rem_lo = s_sel[4];
     for (int i = tid; i < 2048; i += kTopkThreads) hist[i] = 0;
     __syncthreads();
     for (int base = 0; base < S; base += kTopkThreads) {
@@ -294,9 +355,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
     select_bin<kTopkThreads>(hist + 1024, 1024, rem_lo, s_warp, s_sel);
     const uint32_t lo22 = open_bottom ? 0u : (((uint32_t)bin_lo << 10) | (uint32_t)s_sel[0]);
     TK_STAMP(2);
-    // ---- 2. count above / collect candidates
+    // ---- 2. count above / collect candidates into per-warp lists
     {
-      int n_above = 0;
+      int n_above = 0, wn = 0;
+      uint32_t* wk = wc_key + warp * kWarpCand;
+      int* wi = wc_idx + warp * kWarpCand;
       for (int base = 0; base < cols; base += kTopkThreads) {
         const int i = base + tid;
         const uint32_t u = i < cols ? key_at(i) : 0u;
@@ -305,23 +368,36 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
         const bool cand = i < cols && t22 >= lo22 && t22 <= hi22;
         n_above += __popc(__ballot_sync(0xffffffffu, above));
         const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-        if (bal) {
-          const int leader = __ffs(bal) - 1;
-          int slot = 0;
-          if (lane == leader) slot = atomicAdd(&s_nc, __popc(bal));
-          slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(bal & ((1u << lane) - 1u));
-          if (cand && slot < kMaxCand) {
-            cand_key[slot] = u;
-            cand_idx[slot] = i;
-          }
+        const int slot = wn + __popc(bal & ((1u << lane) - 1u));
+        if (cand && slot < kWarpCand) {
+          wk[slot] = u;
+          wi[slot] = i;
         }
+        wn += __popc(bal);
       }
-      if (lane == 0) atomicAdd(&s_na, n_above);
+      if (lane == 0) {
+        s_wn[warp] = wn;
+        atomicAdd(&s_na, n_above);
+        if (wn > kWarpCand) s_ovf = 1;
+      }
     }
     __syncthreads();
-    TK_STAMP(3);
-    const int n_above = s_na, n_cand = s_nc;
-    if (n_above < p.k && n_above + n_cand >= p.k && n_cand <= kMaxCand) {
+    int n_cand = 0, my_off = 0;
+    for (int w = 0; w < kTopkWarps; ++w) {
+      const int c = s_wn[w];
+      if (w < warp) my_off += c;
+      n_cand += c;
+    }
+    const int n_above = s_na;
+    if (!s_ovf && n_above < p.k && n_above + n_cand >= p.k) {
+      // compact the per-warp lists (each warp copies its own)
+      const int wn = s_wn[warp];
+      for (int j = lane; j < wn; j += 32) {
+        cand_key[my_off + j] = wc_key[warp * kWarpCand + j];
+        cand_idx[my_off + j] = wc_idx[warp * kWarpCand + j];
+      }
+      __syncthreads();
+      TK_STAMP(3);
       // ---- 3. exact k-th key among the candidates, then the tie column
       int n_eq, rem;
       prefix = list_select<kTopkThreads>(cand_key, n_cand, p.k - n_above, hist, s_warp, s_sel, &n_eq, &rem);
@@ -381,7 +457,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       bool take = false;
       if (e < cols) {
         if (threshold) {
-          take = __ldg(x + e) > p.thr;
+          take = logit(e) > p.thr;
         } else {
           const uint32_t u = key_at(e);
           take = u > prefix || (u == prefix && e < tie_lim);
@@ -459,7 +535,8 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
     if (!s_last) return;
     __threadfence();
     const uint32_t* gb = p.row_bits + (size_t)g * kGroupRows * words;
-    for (int w = tid; w < words; w += kTopkThreads) p.group_bits[(size_t)g * words + w] = or_rows(gb, g_rows, words, w);
+    for (int w = tid; w < words; w += kTopkThreads)
+      p.group_bits[(size_t)g * words + w] = or_rows<kGroupRows>(gb, g_rows, words, w);
     if (tid == 0) p.tickets[g] = 0;
     __threadfence();
     __syncthreads();
@@ -468,15 +545,19 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
     if (!s_last) return;
     __threadfence();
     const uint32_t* gbits = p.group_bits;
-    compact_words<kTopkThreads>([&](int w) { return or_rows(gbits, groups, words, w); }, p.lo, p.hi, p.pad,
-                                p.union_out, p.count_out, s_warp);
+    if (groups <= 4)
+      compact_words<kTopkThreads>([&](int w) { return or_rows<4>(gbits, groups, words, w); }, p.lo, p.hi, p.pad,
+                                  p.union_out, p.count_out, s_warp);
+    else
+      compact_words<kTopkThreads>([&](int w) { return or_rows<kMaxGroups>(gbits, groups, words, w); }, p.lo, p.hi,
+                                  p.pad, p.union_out, p.count_out, s_warp);
     if (tid == 0) p.tickets[groups] = 0;
     TK_STAMP(6);
   }
 }
 
 size_t topk_smem(int cols, bool threshold) {
-  size_t b = (size_t)4096 * 4 + (size_t)kMaxCand * 4 * 3;
+  size_t b = (size_t)4096 * 4 + (size_t)kMaxCand * 4 * 5;
   if (!threshold && cols <= kTopkSmemCols) b += (size_t)cols * 4;
   return b;
 }
@@ -493,11 +574,12 @@ int launch_topk(TopkParams prm, cudaStream_t st) {
       return PS_ERR_CUDA;
     configured = 1;
   }
-  topk_rows_kernel<<<prm.rows, kTopkThreads, smem, st>>>(prm);
-  return launch_status();
+  return launch_ex(topk_rows_kernel, dim3(prm.rows), dim3(kTopkThreads), smem, st, 1, prm);
 }
 
 __global__ void union_rows_kernel(const int32_t* __restrict__ ids, int n, int width, uint32_t* __restrict__ bitmap) {
+  griddep_wait();
+  griddep_launch();
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const int i = ids[e];
     if (i >= 0 && i < width) atomicOr(bitmap + (i >> 5), 1u << (i & 31));
@@ -514,6 +596,8 @@ __global__ void __launch_bounds__(kCompactThreads) bitmap_compact_kernel(uint32_
                                                                          int32_t* __restrict__ count_out) {
   __shared__ int s_warp[32];
   __shared__ int s_total;
+  griddep_wait();
+  griddep_launch();
   const int words = (width + 31) >> 5;
   const int wlo = lo >> 5, whi = (hi + 31) >> 5;
   const int nw = whi - wlo;
@@ -574,6 +658,8 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
   __shared__ float s_part[kHrWarps * 2][kHrMaxRows];         // per-item partial sums
   uint16_t* sx = reinterpret_cast<uint16_t*>(smem);          // [R][d]
   const int crank = (int)cluster_rank(), csize = (int)cluster_size();
+  griddep_wait();
+  griddep_launch();
   const int r0 = (blockIdx.x / csize) * R;
   const int nr = min(R, B - r0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -682,21 +768,8 @@ int launch_head_router(const uint16_t* x, int64_t x_ld, const uint16_t* w_t, con
   const int csize = H < 8 ? H : 8;
   const int HB = (H + csize - 1) / csize;
   const int groups = (B + R - 1) / R;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(groups * csize);
-  cfg.blockDim = dim3(kHrThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, x, x_ld, w_t, bias, B, d, H, HB, k, logits_out, sel_out) != cudaSuccess)
-    return PS_ERR_CUDA;
-  return launch_status();
+  return launch_ex(kern, dim3(groups * csize), dim3(kHrThreads), smem, st, csize, x, x_ld, w_t, bias, B, d, H, HB, k,
+                   logits_out, sel_out);
 }
 
 }  // namespace
@@ -733,15 +806,17 @@ extern "C" size_t ps_select_union_workspace_bytes(int rows, int cols) {
   return head + (su_groups(rows) + (size_t)rows) * su_words(cols) * 4;
 }
 
-extern "C" int ps_select_union(const float* logits, int rows, int cols, int64_t ld, int k, float thr, void* ws,
-                               size_t ws_bytes, int lo, int hi, int pad, int32_t* union_out, int32_t* count_out,
-                               void* stream) {
+extern "C" int ps_select_union(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k,
+                               float thr, void* ws, size_t ws_bytes, int lo, int hi, int pad, int32_t* union_out,
+                               int32_t* count_out, void* stream) {
   if (rows < 1 || cols < 1 || ld < cols || k > cols || !logits || !ws || !union_out || !count_out)
     return PS_ERR_VALUE;
+  if (rows > kGroupRows * kMaxGroups) return PS_ERR_UNSUPPORTED;
   if (lo < 0 || lo % 32 || hi > cols || hi <= lo || pad < 1) return PS_ERR_VALUE;
   if (ws_bytes < ps_select_union_workspace_bytes(rows, cols)) return PS_ERR_WORKSPACE;
   TopkParams prm{};
   prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k > 0 ? k : 0; prm.thr = thr;
+  prm.bias = bias;
   const size_t tickets = (su_groups(rows) + 1) * 4;
   const size_t head = (tickets + 255) / 256 * 256;
   uint8_t* base = static_cast<uint8_t*>(ws);
@@ -760,17 +835,16 @@ extern "C" int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width
   const int n = rows * k;
   int grid = (n + 255) / 256;
   if (grid > 1184) grid = 1184;
-  union_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows_idx, n, width, bitmap);
-  return launch_status();
+  return launch_ex(union_rows_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 1, rows_idx, n,
+                   width, bitmap);
 }
 
 extern "C" int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, int pad, int32_t* idx_out,
                                  int32_t* count_out, void* stream) {
   if (width < 1 || !bitmap || !idx_out || !count_out || pad < 1) return PS_ERR_VALUE;
   if (lo < 0 || lo % 32 || hi > width || hi <= lo) return PS_ERR_VALUE;
-  bitmap_compact_kernel<<<1, kCompactThreads, 0, static_cast<cudaStream_t>(stream)>>>(bitmap, width, lo, hi, pad,
-                                                                                      idx_out, count_out);
-  return launch_status();
+  return launch_ex(bitmap_compact_kernel, dim3(1), dim3(kCompactThreads), 0, static_cast<cudaStream_t>(stream), 1,
+                   bitmap, width, lo, hi, pad, idx_out, count_out);
 }
 
 extern "C" int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const float* bias, int B, int d,

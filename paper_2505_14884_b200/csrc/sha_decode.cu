@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   const int warp = tid >> 5, lane = tid & 31;
   const int n_units = p.B * p.top_k;
   const int bid = blockIdx.x;
+  griddep_wait();  // q / KV / sel / lengths come from the preceding launches
+  griddep_launch();
 
   if (bid >= n_units * p.splits) {
     // ---- zero-fill CTA for sequence b: heads of non-selected groups = 0.0
@@ -332,8 +334,7 @@ int launch_sha(const ShaParams& prm, int grid, cudaStream_t st) {
       return PS_ERR_CUDA;
     configured = true;
   }
-  kern<<<grid, kThreads, smem, st>>>(prm);
-  return launch_status();
+  return launch_ex(kern, dim3(grid), dim3(kThreads), smem, st, 1, prm);
 }
 
 template <int D_H, int G>

@@ -322,20 +322,25 @@ class DecodeEngine:
             pending = None
             if self.sparse_mlp:
                 r = self.mlp_routers[ell]
+                out_bias = None  # the router's output bias is added inside ps_select_union
                 if self.dense_backend == "cublas":
                     n += self._linear_bf16(self.h, r.w_in_t, r.b_in, self.r_hid, act_relu=True)
-                    n += self._linear_f32(self.r_hid, r.w_out_t, r.b_out, self.r_logits)
+                    torch.mm(self.r_hid, r.w_out_t.t(), out_dtype=torch.float32, out=self.r_logits)
+                    out_bias = r.b_out
                 else:
                     r.logits_into(self.h, self.r_hid, self.r_logits)
                     n += 2
                 lo, hi = (0, cfg.ffn_dim) if self.tp is None else self.tp.ffn_range
-                _lib.check(L.ps_select_union(_lib.ptr(self.r_logits), B, cfg.ffn_dim, cfg.ffn_dim,
+                _lib.check(L.ps_select_union(_lib.ptr(self.r_logits), _lib.ptr(out_bias), B, cfg.ffn_dim, cfg.ffn_dim,
                                              self.k_mlp[ell], 0.0, _lib.ptr(self.su_ws), self.su_bytes,
                                              lo, hi, ROW_PAD, _lib.ptr(self.union_idx),
                                              _lib.ptr(self.union_count), st), "ps_select_union")
                 n += 1
                 if self.record is not None:
-                    self.record.setdefault("mlp_logits", []).append(self.r_logits.clone())
+                    lg = self.r_logits.clone()
+                    if out_bias is not None:
+                        lg += out_bias
+                    self.record.setdefault("mlp_logits", []).append(lg)
                     self.record.setdefault("union", []).append(
                         self.union_idx[: int(self.union_count.item())].clone())
                 if self.tp is None:

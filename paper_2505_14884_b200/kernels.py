@@ -243,7 +243,7 @@ def selective_head_flash_attention_decode(q, cache: KVCache, batch_head_index: B
 # ---------------------------------------------------------------------------
 
 def gather_gemm_into(w_rows, idx, count, x, x_ld, bias, N, M, K, act, out, out_ld,
-                     residual=None, res_ld=0, splits=0, tag="gg_up"):
+                     residual=None, res_ld=0, splits=0, tag="gg_up", flags=0):
     """Raw rows-form launch (see include/polar_b200.h ps_gather_gemm)."""
     lib = _lib.load()
     if splits <= 0:
@@ -252,12 +252,12 @@ def gather_gemm_into(w_rows, idx, count, x, x_ld, bias, N, M, K, act, out, out_l
     dt = _lib.PS_DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.PS_DTYPE_F32
     _lib.call("ps_gather_gemm", _lib.ptr(w_rows), w_rows.shape[0], _lib.ptr(idx), _lib.ptr(count), _lib.ptr(x),
               int(x_ld),
-              _lib.ptr(bias), _lib.ptr(residual), int(res_ld), N, M, K, act, splits, _lib.ptr(out),
+              _lib.ptr(bias), _lib.ptr(residual), int(res_ld), N, M, K, act, splits, flags, _lib.ptr(out),
               int(out_ld), dt, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
 
 
 def gather_gemm_t_into(w_rows, idx, count, h, h_ld, bias, N, M, K_max, out, out_ld,
-                       residual=None, res_ld=0, splits=0, tag="gg_down"):
+                       residual=None, res_ld=0, splits=0, tag="gg_down", flags=0):
     """Raw contraction-form launch (ps_gather_gemm_t)."""
     lib = _lib.load()
     if splits <= 0:
@@ -266,7 +266,7 @@ def gather_gemm_t_into(w_rows, idx, count, h, h_ld, bias, N, M, K_max, out, out_
     dt = _lib.PS_DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.PS_DTYPE_F32
     _lib.call("ps_gather_gemm_t", _lib.ptr(w_rows), w_rows.shape[0], _lib.ptr(idx), _lib.ptr(count), _lib.ptr(h),
               int(h_ld),
-              _lib.ptr(bias), _lib.ptr(residual), int(res_ld), N, M, K_max, splits, _lib.ptr(out),
+              _lib.ptr(bias), _lib.ptr(residual), int(res_ld), N, M, K_max, splits, flags, _lib.ptr(out),
               int(out_ld), dt, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
 
 
@@ -356,7 +356,8 @@ def mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor,
     gather_gemm_t_into(pk.w2t, idx, count, hidden, hidden.stride(0), pk.b2, B, d,
                        pk.D if idx is None else pk.D_pad, out, out.stride(0),
                        residual=residual, res_ld=0 if residual is None else residual.stride(0),
-                       splits=splits_down or expected, tag="gg_down")
+                       splits=splits_down or expected, tag="gg_down",
+                       flags=_lib.PS_GG_A_READY)  # idx/count were written before the UP launch
 
 
 def sparse_mlp_forward(x, w1, b1=None, w2=None, b2=None, active=None) -> torch.Tensor:

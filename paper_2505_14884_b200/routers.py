@@ -204,7 +204,7 @@ def union_from_logits(logits: torch.Tensor, k: int | None = None, threshold: flo
     ws = _ws.get(f"select_union_{rows}_{width}", nbytes, dev)
     buf = torch.empty(_round_up(width, ROW_PAD), dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.call("ps_select_union", _lib.ptr(logits), rows, width, width, int(k) if k is not None else 0,
+    _lib.call("ps_select_union", _lib.ptr(logits), None, rows, width, width, int(k) if k is not None else 0,
               float(threshold or 0.0), _lib.ptr(ws), nbytes, 0, width, ROW_PAD, _lib.ptr(buf),
               _lib.ptr(cnt), _lib.stream_ptr())
     return NeuronIndexTensor(layer, buf, cnt)

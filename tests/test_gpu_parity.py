@@ -112,6 +112,29 @@ def test_topk_union_cluster_shapes(rows):
     assert np.array_equal(got, po.topk_indices_rows(s, cols // 10))
 
 
+def test_select_union_with_bias():
+    """ps_select_union adds the router's output bias (routers.py:286-288)
+    while staging: identical to selecting on logits + bias."""
+    from paper_2505_14884_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    rows, cols, k = 40, 8192, 1000
+    s = rng.normal(size=(rows, cols)).astype(np.float32)
+    b = (rng.normal(size=cols) * 3).astype(np.float32)
+    ref = po.union_neuron_indices(list(po.topk_indices_rows((s + b).astype(np.float32), k)))
+    L = _lib.load()
+    nb = int(L.ps_select_union_workspace_bytes(rows, cols))
+    ws = torch.zeros(nb, dtype=torch.uint8, device=DEV)
+    buf = torch.empty(cols, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(1, dtype=torch.int32, device=DEV)
+    lg, bt = t(s), t(b)
+    for _ in range(2):  # self-resetting tickets: a second call must agree
+        _lib.call("ps_select_union", _lib.ptr(lg), _lib.ptr(bt), rows, cols, cols, k, 0.0, _lib.ptr(ws), nb, 0,
+                  cols, 128, _lib.ptr(buf), _lib.ptr(cnt), _lib.stream_ptr())
+        n = int(cnt.item())
+        assert np.array_equal(buf[:n].cpu().numpy(), ref)
+
+
 def test_union_bit_exact(golden):
     for i in range(int(golden["union_n"])):
         rows = golden[f"union_rows_{i}"]

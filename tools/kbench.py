@@ -123,7 +123,7 @@ def main():
         buf = torch.empty(D, dtype=torch.int32, device=dev)
         cnt = torch.zeros(1, dtype=torch.int32, device=dev)
         st = lambda: _lib.stream_ptr()  # noqa
-        f = lambda i: _lib.call("ps_select_union", logits.data_ptr(), B, D, D, int(a.union * D), 0.0, ws.data_ptr(),  # noqa
+        f = lambda i: _lib.call("ps_select_union", logits.data_ptr(), None, B, D, D, int(a.union * D), 0.0, ws.data_ptr(),  # noqa
                                 nb, 0, D, 128, buf.data_ptr(), cnt.data_ptr(), st())
         rep(f"select_union (topk+union+compact) {B}x{D} k={int(a.union * D)}", timeit(f, a.iters), B * D * 4)
         hr = pb.HeadRouter(d, 32, seed=1)

@@ -22,7 +22,7 @@ for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 16384, 8192, "normal"
     ids = torch.empty(rows, k, dtype=torch.int32, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
     tk = torch.zeros(1, dtype=torch.int32, device=dev)
-    f_union = lambda i: _lib.call("ps_select_union", lg.data_ptr(), rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
+    f_union = lambda i: _lib.call("ps_select_union", lg.data_ptr(), None, rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
                                   nb, 0, cols, 128, buf.data_ptr(), cnt.data_ptr(), st())
     f_bm = lambda i: _lib.call("ps_topk_rows", lg.data_ptr(), rows, cols, cols, k, None, bm.data_ptr(), st())  # noqa
     f_ids = lambda i: _lib.call("ps_topk_rows", lg.data_ptr(), rows, cols, cols, k, ids.data_ptr(), None, st())  # noqa

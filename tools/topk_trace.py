@@ -20,7 +20,7 @@ for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"),
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
     tk = torch.zeros(1, dtype=torch.int32, device=dev)
     tr = torch.zeros(rows * 8 * 16, dtype=torch.int64, device=dev)
-    f = lambda: _lib.call("ps_select_union", lg.data_ptr(), rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
+    f = lambda: _lib.call("ps_select_union", lg.data_ptr(), None, rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
                           nb, 0, cols, 128, buf.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
     for _ in range(3):
         f()
