@@ -72,6 +72,8 @@ int ps_num_sms(void);
  *   ws      >= ps_sha_workspace_bytes(...) bytes; must be zero-filled
  *           before its first use (the kernel leaves it zeroed again)
  * ==================================================================== */
+/* debug: 0 forces the CUDA-core SHA path (d_h = 128 otherwise runs on mma.sync) */
+void ps_debug_sha_mma(int enable);
 size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int top_k, int num_splits);
 int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_len);
 int ps_sha_decode(const void* q, int64_t q_ld,

@@ -21,6 +21,10 @@
 //     registers/smem, per-split (m, l, o) partials merged by the last CTA of
 //     the unit (atomic ticket; counters self-reset, so the call is graph-safe);
 //   * B extra CTAs write the exact zeros of the non-selected heads.
+#include <cmath>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace ps {
@@ -393,6 +397,371 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   griddep_launch();
 }
 
+// ============================================================================
+// Tensor-core SHA (d_h = 128, G <= 8).  Same stream-K partition and merge as
+// above, but the per-tile math runs on mma.sync: each warp owns 8 KV rows of
+// a 32-row tile; S = Q K^T with m16n8k16 (the G query heads are the M rows,
+// zero-padded to 16), online softmax on the S fragment (the 4 lanes of a
+// head shuffle-reduce its row max), P (bf16) V with m16n8k8 into a 16 x 128
+// f32 accumulator.  K/V tiles arrive through 2-D TMA boxes (32 rows x 64
+// dims) with the 128-byte swizzle, so the ldmatrix reads of 8 rows at one
+// column chunk are bank-conflict free.  ~80 instructions per warp per tile
+// (vs ~280 for the CUDA-core path), so the kernel streams at HBM rate.
+// Rows past a sequence's length inside its last tile are loaded (the box is
+// fixed) but never used: their scores are masked by select and their V rows
+// are zeroed in shared memory before the P.V product.
+constexpr int kMmaT = 32;
+constexpr int kMmaStages = 4;
+constexpr int kMmaTileBytes = kMmaT * 128 * 2;  // 8 KB of K (or V)
+
+PS_DEV void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+PS_DEV void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+PS_DEV void mma_16816(float* d, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  // A rows 8..15 (a1, a3) are the zero padding of the G <= 8 heads
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+PS_DEV void mma_1688(float* d, uint32_t a0, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(b0));
+}
+// byte offset of 16-byte chunk C (0..15) of tile row r in a swizzled K/V tile
+PS_DEV uint32_t mma_sw(int r, int C) {
+  return (uint32_t)((C >> 3) * 4096 + r * 128 + (((C & 7) ^ (r & 7)) << 4));
+}
+
+template <int G, bool OUT_BF16>
+__global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant__ CUtensorMap tmK,
+                                                          const __grid_constant__ CUtensorMap tmV, const ShaParams p) {
+  constexpr int D_H = 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + kMmaStages * kMmaTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kMmaStages * kMmaTileBytes);
+  float* red = reinterpret_cast<float*>(smem + 2 * kMmaStages * kMmaTileBytes + 64);
+  float* red_m = red;                 // [kWarps][G]
+  float* red_l = red + kWarps * G;    // [kWarps][G]
+  float* red_o = red + 2 * kWarps * G;  // [kWarps][G][D_H]
+  int* flag = reinterpret_cast<int*>(red + kWarps * G * (D_H + 2));
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int n_units = p.B * p.top_k;
+  const int bid = blockIdx.x;
+  griddep_wait();
+
+  if (bid >= p.n_ctas) {
+    // ---- zero-fill CTA for sequence b: heads of non-selected groups = 0.0
+    const int b = bid - p.n_ctas;
+    int* sel_flag = reinterpret_cast<int*>(smem);
+    for (int g = tid; g < p.H_kv; g += kThreads) sel_flag[g] = 0;
+    __syncthreads();
+    for (int j = tid; j < p.top_k; j += kThreads) {
+      int g = p.sel[(size_t)b * p.top_k + j] - p.group_base;
+      if (g >= 0 && g < p.H_kv) sel_flag[g] = 1;
+    }
+    __syncthreads();
+    const int total = p.H * D_H;
+    for (int e = tid; e < total; e += kThreads) {
+      int grp = (e / D_H) / G;
+      if (!sel_flag[grp]) store_out<OUT_BF16>(p.out, (size_t)b * p.out_ld + e, 0.0f);
+    }
+    griddep_launch();
+    return;
+  }
+
+  const long long F = (long long)n_units * p.NT;
+  const long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
+  const int n_it = (int)(f1 - f0);
+  const int u_first = n_it > 0 ? (int)(f0 / p.NT) : 0;
+  const int sel_first = __ldg(p.sel + u_first);
+  const int len_first = __ldg(p.lengths + u_first / p.top_k);
+  if (tid == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    for (int s = 0; s < kMmaStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // producer cursor (thread 0)
+  struct Cursor {
+    int u, t, len, row_base;
+    bool live;
+  } cur;
+  auto load_unit = [&](int u) {
+    cur.u = u;
+    const int b = u / p.top_k;
+    const int g = (u == u_first ? sel_first : __ldg(p.sel + u)) - p.group_base;
+    cur.live = g >= 0 && g < p.H_kv;
+    cur.len = u == u_first ? len_first : __ldg(p.lengths + b);
+    cur.row_base = (b * p.H_kv + (cur.live ? g : 0)) * p.cap;
+  };
+  auto issue_next = [&](int stage) {
+    const int row0 = cur.t * kMmaT;
+    if (!cur.live || row0 >= cur.len) {
+      mbar_arrive(&bars[stage]);
+    } else {
+      mbar_arrive_expect_tx(&bars[stage], 2 * kMmaTileBytes);
+      uint8_t* k_dst = sK + stage * kMmaTileBytes;
+      uint8_t* v_dst = sV + stage * kMmaTileBytes;
+      tma_load_2d(k_dst, &tmK, 0, cur.row_base + row0, &bars[stage]);
+      tma_load_2d(k_dst + 4096, &tmK, 64, cur.row_base + row0, &bars[stage]);
+      tma_load_2d(v_dst, &tmV, 0, cur.row_base + row0, &bars[stage]);
+      tma_load_2d(v_dst + 4096, &tmV, 64, cur.row_base + row0, &bars[stage]);
+    }
+    if (++cur.t == p.NT) {
+      cur.t = 0;
+      if (cur.u + 1 < n_units) load_unit(cur.u + 1);
+    }
+  };
+  if (tid == 0 && n_it > 0) {
+    load_unit(u_first);
+    cur.t = (int)(f0 - (long long)u_first * p.NT);
+    const int pre = min(kMmaStages, n_it);
+    for (int s2 = 0; s2 < pre; ++s2) issue_next(s2);
+  }
+
+  const int gq = lane >> 2;         // head (M row) of this lane's fragments
+  const int kq = (lane & 3) * 2;    // column pair inside an 8-wide block
+  const int lrow = warp * 8 + (lane & 7);  // ldmatrix row supplied by this lane
+  const int lmat = lane >> 3;              // ldmatrix matrix index
+  const uint32_t sK_u = smem_u32(sK), sV_u = smem_u32(sV);
+  int it = 0;
+  long long f = f0;
+  while (f < f1) {
+    const int u = (int)(f / p.NT);
+    const long long u_end = (long long)(u + 1) * p.NT;
+    const long long seg_end = f1 < u_end ? f1 : u_end;
+    const int b = u / p.top_k;
+    const int g = (u == u_first ? sel_first : __ldg(p.sel + u)) - p.group_base;
+    const bool live = g >= 0 && g < p.H_kv;
+    const int len = u == u_first ? len_first : __ldg(p.lengths + b);
+    const int nt_seg = (int)(seg_end - f);
+    const int t0 = (int)(f - (long long)u * p.NT);
+    f = seg_end;
+    if (!live) {
+      for (int k2 = 0; k2 < nt_seg; ++k2, ++it) {
+        const int stage = it % kMmaStages;
+        mbar_wait(&bars[stage], (it / kMmaStages) & 1);
+        __syncthreads();
+        if (tid == 0 && it + kMmaStages < n_it) issue_next(stage);
+      }
+      continue;
+    }
+    // Q fragments (rows = heads; heads >= G are zero)
+    uint32_t qa[8][2];
+    {
+      const uint16_t* qb = p.q + (size_t)b * p.q_ld + (size_t)g * G * D_H;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (gq < G) {
+          qa[j][0] = *reinterpret_cast<const uint32_t*>(qb + gq * D_H + 16 * j + kq);
+          qa[j][1] = *reinterpret_cast<const uint32_t*>(qb + gq * D_H + 16 * j + 8 + kq);
+        } else {
+          qa[j][0] = qa[j][1] = 0u;
+        }
+      }
+    }
+    float m_run = -INFINITY, l_run = 0.f;
+    float o[16][4];
+#pragma unroll
+    for (int nb = 0; nb < 16; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+    const int nt_real = max(0, min(nt_seg, (len + kMmaT - 1) / kMmaT - t0));
+    for (int k2 = 0; k2 < nt_seg; ++k2, ++it) {
+      const int stage = it % kMmaStages;
+      mbar_wait(&bars[stage], (it / kMmaStages) & 1);
+      if (k2 < nt_real) {
+        const int valid = min(kMmaT, len - (t0 + k2) * kMmaT);
+        const uint32_t kbase = sK_u + stage * kMmaTileBytes, vbase = sV_u + stage * kMmaTileBytes;
+        if (valid < kMmaT && warp * 8 + 8 > valid) {
+          // rows past the length in this warp's slice: zero their V (never used, maybe NaN)
+          uint8_t* vt = sV + stage * kMmaTileBytes;
+          for (int e = lane; e < 8 * 16; e += 32) {
+            const int r = warp * 8 + (e >> 4), C = e & 15;
+            if (r >= valid) *reinterpret_cast<uint4*>(vt + mma_sw(r, C)) = make_uint4(0, 0, 0, 0);
+          }
+          fence_proxy_async();  // generic writes before the next TMA into this stage
+          __syncwarp();
+        }
+        // ---- S = Q K^T for this warp's 8 rows (two accumulators: shorter MMA chain)
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t kb[4];
+          ldsm_x4(kbase + mma_sw(lrow, 4 * i + lmat), kb);
+          mma_16816(sa, qa[2 * i][0], qa[2 * i][1], kb[0], kb[1]);
+          mma_16816(sb, qa[2 * i + 1][0], qa[2 * i + 1][1], kb[2], kb[3]);
+        }
+        const int r0 = warp * 8 + kq;
+        float s0 = (sa[0] + sb[0]) * p.scale_log2, s1 = (sa[1] + sb[1]) * p.scale_log2;
+        s0 = r0 < valid ? s0 : -INFINITY;
+        s1 = r0 + 1 < valid ? s1 : -INFINITY;
+        float mx = fmaxf(s0, s1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        const float alpha = fast_exp2(m_run - m_use);
+        const float p0 = fast_exp2(s0 - m_use), p1 = fast_exp2(s1 - m_use);
+        l_run = l_run * alpha + p0 + p1;
+        m_run = m_new;
+        const uint32_t pa = pack_bf16x2(p0, p1);
+        // ---- O = O * alpha + P V
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t vb[4];
+          ldsm_x4_t(vbase + mma_sw(lrow, 4 * i + lmat), vb);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            float* acc = o[4 * i + m];
+            acc[0] *= alpha;
+            acc[1] *= alpha;
+            mma_1688(acc, pa, vb[m]);
+          }
+        }
+      }
+      __syncthreads();  // every warp is done with this stage
+      if (tid == 0 && it + kMmaStages < n_it) issue_next(stage);
+    }
+
+    // ---- per-warp state -> shared (lanes of head gq own dims 8nb + kq, +1)
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    if (gq < G) {
+#pragma unroll
+      for (int nb = 0; nb < 16; ++nb) {
+        red_o[(warp * G + gq) * D_H + 8 * nb + kq] = o[nb][0];
+        red_o[(warp * G + gq) * D_H + 8 * nb + kq + 1] = o[nb][1];
+      }
+      if ((lane & 3) == 0) {
+        red_m[warp * G + gq] = m_run;
+        red_l[warp * G + gq] = l_run;
+      }
+    }
+    __syncthreads();
+
+    // ---- merge warps; a unit inside one CTA writes its output directly
+    const int c_first = cta_of((long long)u * p.NT, F, p.n_ctas);
+    const int c_last = cta_of(u_end - 1, F, p.n_ctas);
+    const int nseg = c_last - c_first + 1, seg = bid - c_first;
+    const size_t out_row = (size_t)b * p.out_ld + (size_t)g * G * D_H;
+    const int stride = G * (D_H + 2);
+    float* part = p.partials + ((size_t)u * p.max_seg + seg) * (size_t)stride;
+    for (int e = tid; e < G * D_H; e += kThreads) {
+      const int h = e / D_H;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red_m[w * G + h]);
+      float L = 0.f, O = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const float mw = red_m[w * G + h];
+        const float wt = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
+        L += red_l[w * G + h] * wt;
+        O += red_o[(w * G) * D_H + e] * wt;
+      }
+      if (nseg == 1) {
+        store_out<OUT_BF16>(p.out, out_row + e, O / L);
+      } else {
+        part[2 * G + e] = O;
+        if ((e % D_H) == 0) {
+          part[h] = M;
+          part[G + h] = L;
+        }
+      }
+    }
+    if (nseg > 1) {
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const int prev = atomicAdd(&p.counters[u], 1);
+        *flag = (prev == nseg - 1);
+      }
+      __syncthreads();
+      if (*flag) {
+        __threadfence();
+        const float* base = p.partials + (size_t)u * p.max_seg * (size_t)stride;
+        for (int e = tid; e < G * D_H; e += kThreads) {
+          const int h = e / D_H;
+          float M = -INFINITY;
+          for (int s2 = 0; s2 < nseg; ++s2) M = fmaxf(M, __ldcg(base + s2 * stride + h));
+          float L = 0.f, O = 0.f;
+          for (int s2 = 0; s2 < nseg; ++s2) {
+            const float ms = __ldcg(base + s2 * stride + h);
+            const float wt = (ms == -INFINITY) ? 0.f : fast_exp2(ms - M);
+            L += __ldcg(base + s2 * stride + G + h) * wt;
+            O += __ldcg(base + s2 * stride + 2 * G + e) * wt;
+          }
+          store_out<OUT_BF16>(p.out, out_row + e, O / L);
+        }
+        if (tid == 0) p.counters[u] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  griddep_launch();
+}
+
+template <int G>
+constexpr size_t sha_mma_smem_bytes() {
+  return 1024 + 2 * kMmaStages * kMmaTileBytes + 64 + (size_t)kWarps * G * (128 + 2) * 4 + 16;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_sha_encode = nullptr;
+
+int sha_tmap(CUtensorMap* m, const void* base, uint64_t rows) {
+  if (!g_sha_encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return PS_ERR_CUDA;
+    g_sha_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {128, rows};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {64, (cuuint32_t)kMmaT};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_sha_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? PS_OK : PS_ERR_VALUE;
+}
+
+template <int G, bool BF16>
+int launch_sha_mma(const ShaParams& prm, int grid, cudaStream_t st) {
+  constexpr size_t smem = sha_mma_smem_bytes<G>();
+  auto kern = sha_mma_kernel<G, BF16>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return PS_ERR_CUDA;
+    configured = true;
+  }
+  const uint64_t rows = (uint64_t)prm.B * prm.H_kv * prm.cap;
+  CUtensorMap tk, tv;
+  int rc = sha_tmap(&tk, prm.k, rows);
+  if (rc == PS_OK) rc = sha_tmap(&tv, prm.v, rows);
+  if (rc != PS_OK) return rc;
+  return launch_ex(kern, dim3(grid), dim3(kThreads), smem, st, 1, tk, tv, prm);
+}
+
+int g_sha_mma = 1;  // 0: CUDA-core path for every shape (ps_debug_sha_mma)
+
 template <int D_H, int G, bool BF16>
 int launch_sha(const ShaParams& prm, int grid, cudaStream_t st) {
   constexpr size_t smem = sha_smem_bytes<D_H, G>();
@@ -429,10 +798,34 @@ int partial_floats(int G, int d_h) { return G * (d_h + 2); }
 // resident SHA CTAs (64 KB of K/V stages each: 3 per SM)
 int sha_slots() { return ps_num_sms() * 3; }
 
-// stream-K CTAs: num_splits > 0 caps them at units * num_splits (the classic
-// FlashDecoding split count); 0 = one resident wave (every SM streaming)
+// CTAs = units x splits (each unit cut into `splits` equal tile ranges).
+// Auto (num_splits == 0): the split count minimising the last-wave waste
+// ceil(W)/W (W = units*s / resident slots) plus a per-split cost (partials +
+// merge, ~4 % each), with >= 4 tiles per split -- measured on B200 (ctx
+// 1920): s = 1 at 2048 and 256 units, 3 at 1024 (OPT-6.7B B=64 rho=.5), 4 at
+// 512, 2 at 128.
+int sha_auto_splits(int units, int NT) {
+  const double slots = (double)sha_slots();
+  int best = 1;
+  double best_cost = 1e30;
+  for (int s = 1; s <= 8; ++s) {
+    if (s > 1 && NT / s < 4) break;
+    const double n = units * (double)s, w = n / slots;
+    // one partial wave streams at full rate once ~256 CTAs (1.7 per SM) are
+    // in flight; beyond a wave, the last wave's idle fraction is lost
+    const double wave = n <= slots ? (n >= 256.0 ? 1.0 : 256.0 / n) : std::ceil(w) / w;
+    const double cost = wave + 0.04 * s;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
 int sha_ctas(int units, int NT, int num_splits) {
-  long long cap = num_splits > 0 ? (long long)units * num_splits : (long long)sha_slots();
+  if (num_splits <= 0) num_splits = sha_auto_splits(units, NT);
+  long long cap = (long long)units * num_splits;
   const long long F = (long long)units * NT;
   if (cap > F) cap = F;
   return (int)(cap < 1 ? 1 : cap);
@@ -451,9 +844,11 @@ using namespace ps;
 extern "C" size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int top_k, int num_splits) {
   if (B < 1 || H_kv < 1 || top_k < 1 || H % H_kv) return 0;
   const size_t units = (size_t)B * top_k;
-  const int n = num_splits > 0 ? (int)(units * num_splits) : sha_slots();  // upper bound of sha_ctas
+  const int n = (int)(units * (num_splits > 0 ? num_splits : 8));  // upper bound of sha_ctas
   return kCounterBytes + units * (size_t)sha_max_seg((int)units, n) * (size_t)partial_floats(H / H_kv, d_h) * 4;
 }
+
+extern "C" void ps_debug_sha_mma(int enable) { g_sha_mma = enable ? 1 : 0; }
 
 // 0 = stream-K over one resident wave (the default)
 extern "C" int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_len) {
@@ -509,7 +904,17 @@ extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, c
     case 16: return dispatch_g<16>(prm, grid, G, bf16, st);
     case 32: return dispatch_g<32>(prm, grid, G, bf16, st);
     case 64: return dispatch_g<64>(prm, grid, G, bf16, st);
-    case 128: return dispatch_g<128>(prm, grid, G, bf16, st);
+    case 128:
+      if (g_sha_mma && G <= 8 && (((uintptr_t)k_cache | (uintptr_t)v_cache) % 16) == 0) {
+        switch (G) {
+          case 1: return bf16 ? launch_sha_mma<1, true>(prm, grid, st) : launch_sha_mma<1, false>(prm, grid, st);
+          case 2: return bf16 ? launch_sha_mma<2, true>(prm, grid, st) : launch_sha_mma<2, false>(prm, grid, st);
+          case 4: return bf16 ? launch_sha_mma<4, true>(prm, grid, st) : launch_sha_mma<4, false>(prm, grid, st);
+          case 8: return bf16 ? launch_sha_mma<8, true>(prm, grid, st) : launch_sha_mma<8, false>(prm, grid, st);
+          default: break;
+        }
+      }
+      return dispatch_g<128>(prm, grid, G, bf16, st);
     case 256: return dispatch_g<256>(prm, grid, G, bf16, st);
     default: return PS_ERR_UNSUPPORTED;
   }

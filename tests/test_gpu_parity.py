@@ -268,6 +268,47 @@ def test_attention_opt_llama_shapes_vs_oracle(B, H, H_kv, d_h, N, rho):
     assert np.abs(got - ref).max() <= 2e-3
 
 
+@pytest.mark.parametrize("H,H_kv", [(32, 32), (32, 8), (64, 8)])
+def test_attention_tensor_core_path_poison_and_agreement(H, H_kv):
+    """d_h = 128 runs on mma.sync with swizzled TMA tiles: ragged lengths
+    (partial last tiles), NaN past every length and in non-selected groups,
+    agreement with the CUDA-core path and the oracle."""
+    from paper_2505_14884_b200 import _lib
+
+    rng = np.random.default_rng(H + H_kv)
+    B, N, d_h = 6, 300, 128
+    c = pb.KVCache(B, H_kv, N + 40, d_h, device=DEV)
+    c.fill_random(rng, N)
+    lens = np.array([300, 1, 31, 33, 250, 97])
+    c.set_lengths(lens)
+    q = po.round_bf16(rng.normal(size=(B, H, 1, d_h)).astype(np.float32))
+    k = max(1, H_kv // 2)
+    sel = np.stack([np.sort(rng.choice(H_kv, k, replace=False)) for _ in range(B)])
+    bhi = pb.BatchHeadIndex(sel)
+    keys, vals = c.keys.float().cpu().numpy(), c.values.float().cpu().numpy()
+    ref = po.naive_attention_reference(q, keys, vals, lens, sel, H // H_kv)
+    clean = pb.gqa_selective_attention_decode(t(q), c, bhi).cpu()
+    for b in range(B):
+        c.keys[b, :, int(lens[b]):] = float("nan")
+        c.values[b, :, int(lens[b]):] = float("nan")
+        for g in range(H_kv):
+            if g not in sel[b]:
+                c.keys[b, g] = float("nan")
+                c.values[b, g] = float("nan")
+    poisoned = pb.gqa_selective_attention_decode(t(q), c, bhi).cpu()
+    assert torch.isfinite(poisoned).all()
+    assert torch.equal(poisoned, clean)
+    err = np.abs(clean.numpy() - ref)
+    assert err.max() <= 1e-2 and err.mean() <= 1e-3, (err.max(), err.mean())
+    L = _lib.load()
+    L.ps_debug_sha_mma(0)
+    try:
+        core = pb.gqa_selective_attention_decode(t(q), c, bhi).cpu()
+    finally:
+        L.ps_debug_sha_mma(1)
+    assert (core - clean).abs().max().item() <= 1e-2
+
+
 # ----------------------------------------------------------------- MLP / GEMM
 
 def test_mlp_matches_reference(golden):
