@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--kv-ring", type=int, default=0, help="alias KV storage over this many buffers (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
+    ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native"])
     return ap.parse_args()
 
 
@@ -230,6 +231,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(kernel, args):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel`
+    from the committed `ncu --set full` capture of this same workload
+    (tools/gpu_profiles.sh -> profiles/r01_ncu_traffic.json), else None."""
+    if (args.config, args.batch, args.ctx, args.rho, args.union) != ("opt-6.7b", 64, 1920, 0.5, 0.5):
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            doc = json.load(f)
+        for k in doc["kernels"]:
+            if kernel in k["kernel"]:
+                return k["dram_read_bytes"] + k["dram_write_bytes"]
+    except Exception:
+        return None
+    return None
+
+
 def workload_config(args, cfg):
     return {"workload": f"{args.config} polar decode step", "model_shape": args.config, "global_batch": args.batch,
             "seq_len": args.ctx, "head_density": args.rho, "union_density": args.union,
@@ -284,7 +302,8 @@ def run_ours(args):
                                          hot=gen.choice(D, k_mlp, replace=False)) for ell in range(L)]
     polar = SparsityPolicy(mode="polar", head_density=args.rho,
                            mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
-    eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring)
+    eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring,
+                       router_backend=args.router_backend)
     eng.fill_random(ctx, seed=99 + rank)
     dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches)
     tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()
@@ -371,6 +390,7 @@ def run_ours(args):
     sha_bytes = float(np.mean([sha_algorithmic_bytes(l, k_h, H // H_kv, d_h, B, H) for l in lens]))
     hbm_peak, _, peak_kind = load_peaks()
     achieved = sha_bytes / (sha_ms * 1e-3) / 1e9
+    traffic = ncu_traffic("sha_mma_kernel", args)
 
     # selective MLP kernels alone (UP + DOWN gathered GEMMs), one per layer
     mlp_ms = None
@@ -416,8 +436,10 @@ def run_ours(args):
             "e2e": {"value": toks / (ms_e2e * 1e-3), "unit": "tok/s", "h2d_bytes_per_step": B * 4,
                     "d2h_bytes_per_step": B * 8, "wall_ms_per_step": wall_e2e / args.steps},
             "gpu_launches": int(eng.launches_per_step) * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "sha_decode_kernel", "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+            "roofline": {"bound": "hbm", "kernel": "sha_mma_kernel", "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                         "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, same workload)"
+                         if traffic is not None else None,
                          "peak_kind": peak_kind, "bytes_per_launch": sha_bytes, "us_per_launch": sha_ms * 1e3},
             "kernels": {"sparse_mlp_us_per_layer": None if mlp_ms is None else mlp_ms * 1e3,
                         "sparse_mlp_GBps": None if mlp_ms is None else mlp_bytes / (mlp_ms * 1e-3) / 1e9},

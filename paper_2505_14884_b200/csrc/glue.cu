@@ -140,17 +140,32 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const int32_t* __r
     x[(size_t)b * d + i] = __uint_as_float((uint32_t)er[i] << 16) + __uint_as_float((uint32_t)pr[i] << 16);
 }
 
-// h = silu(gate) * up, gate/up from one (B, 2D) bf16 row [gate | up]
+// h = silu(gate) * up, gate/up from one (B, 2D) bf16 row [gate | up]:
+// grid (column blocks, B), 8 columns per thread with 16-byte loads/stores
 __global__ void swiglu_kernel(const uint16_t* __restrict__ gu, int64_t gu_ld, int B, int D,
-                              uint16_t* __restrict__ h, int64_t h_ld) {
+                              uint16_t* __restrict__ h, int64_t h_ld, int vec) {
   griddep_wait();
   griddep_launch();
-  const int64_t total = (int64_t)B * D;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(e / D), j = (int)(e - (int64_t)b * D);
-    const float g = __uint_as_float((uint32_t)gu[(size_t)b * gu_ld + j] << 16);
-    const float u = __uint_as_float((uint32_t)gu[(size_t)b * gu_ld + D + j] << 16);
-    h[(size_t)b * h_ld + j] = f2bf(g / (1.f + __expf(-g)) * u);
+  const int b = blockIdx.y;
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (j0 >= D) return;
+  const uint16_t* gr = gu + (size_t)b * gu_ld;
+  uint16_t* hr = h + (size_t)b * h_ld;
+  if (vec && j0 + 8 <= D) {
+    float g[8], u[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(gr + j0)), g);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(gr + D + j0)), u);
+    uint4 o;
+    o.x = pack_bf16x2(g[0] / (1.f + __expf(-g[0])) * u[0], g[1] / (1.f + __expf(-g[1])) * u[1]);
+    o.y = pack_bf16x2(g[2] / (1.f + __expf(-g[2])) * u[2], g[3] / (1.f + __expf(-g[3])) * u[3]);
+    o.z = pack_bf16x2(g[4] / (1.f + __expf(-g[4])) * u[4], g[5] / (1.f + __expf(-g[5])) * u[5]);
+    o.w = pack_bf16x2(g[6] / (1.f + __expf(-g[6])) * u[6], g[7] / (1.f + __expf(-g[7])) * u[7]);
+    *reinterpret_cast<uint4*>(hr + j0) = o;
+  } else {
+    for (int j = j0; j < min(D, j0 + 8); ++j) {
+      const float g = __uint_as_float((uint32_t)gr[j] << 16), u = __uint_as_float((uint32_t)gr[D + j] << 16);
+      hr[j] = f2bf(g / (1.f + __expf(-g)) * u);
+    }
   }
 }
 
@@ -237,9 +252,10 @@ extern "C" int ps_embed(const int32_t* tokens, const int32_t* lengths, const voi
 
 extern "C" int ps_swiglu(const void* gu, int64_t gu_ld, int B, int D, void* h, int64_t h_ld, void* stream) {
   if (B < 1 || D < 1 || !gu || !h || gu_ld < 2 * (int64_t)D || h_ld < D) return PS_ERR_VALUE;
-  const int64_t total = (int64_t)B * D;
-  int grid = (int)((total + 255) / 256);
-  if (grid > 148 * 16) grid = 148 * 16;
-  return launch_ex(swiglu_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream), 1,
-                   static_cast<const uint16_t*>(gu), gu_ld, B, D, static_cast<uint16_t*>(h), h_ld);
+  // 16-byte vector path needs 8-element aligned rows and halves
+  const int vec = !((gu_ld % 8) || (h_ld % 8) || (D % 8) || ((uintptr_t)gu % 16) || ((uintptr_t)h % 16));
+  const int threads = 128;
+  const dim3 grid((D / 8 + threads - 1) / threads, B);
+  return launch_ex(swiglu_kernel, grid, dim3(threads), 0, static_cast<cudaStream_t>(stream), 1,
+                   static_cast<const uint16_t*>(gu), gu_ld, B, D, static_cast<uint16_t*>(h), h_ld, vec);
 }

@@ -86,12 +86,16 @@ class DecodeEngine:
 
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
-                 caches=None, dense_backend: str = "cublas"):
+                 caches=None, dense_backend: str = "cublas", router_backend: str | None = None):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
         self.model, self.cfg, self.B, self.policy = model, cfg, batch, policy
         self.dense_backend = check_choice(dense_backend, ("cublas", "native"), "dense_backend")
+        # the MLP router's two layers: tcgen05 kernels with their static weights
+        # streamed ahead of the previous launch (PDL), or cuBLAS
+        self.router_backend = check_choice(router_backend or dense_backend, ("cublas", "native"),
+                                           "router_backend")
         self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
         self.tp = tp
@@ -323,7 +327,7 @@ class DecodeEngine:
             if self.sparse_mlp:
                 r = self.mlp_routers[ell]
                 out_bias = None  # the router's output bias is added inside ps_select_union
-                if self.dense_backend == "cublas":
+                if self.router_backend == "cublas":
                     n += self._linear_bf16(self.h, r.w_in_t, r.b_in, self.r_hid, act_relu=True)
                     torch.mm(self.r_hid, r.w_out_t.t(), out_dtype=torch.float32, out=self.r_logits)
                     out_bias = r.b_out
