@@ -45,7 +45,7 @@ PS_DEV int block_excl_scan(int v, int* s_warp, int* total) {
   return before + x - v;
 }
 
-constexpr int kTopkThreads = 1024;
+constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int kTopkSmemCols = 40960;  // rows up to this width are staged in shared memory (160 KB)
 constexpr int kSample = 2048;         // strided sample of a row that brackets the k-th key
@@ -65,7 +65,8 @@ struct TopkParams {
   // fused union (ps_select_union): per-row words, per-group words, tickets
   uint32_t* row_bits;    // (rows, words) or NULL
   uint32_t* group_bits;  // (groups, words)
-  int* tickets;          // [groups] + [1] (self-resetting)
+  int* tickets;          // [groups] + [1] + barrier {count, gen} + [rows] totals (self-resetting)
+  int coresident;        // every row CTA is resident at once: grid barrier + distributed union
   int lo, hi, pad;
   int32_t* union_out;
   int32_t* count_out;
@@ -250,7 +251,9 @@ PS_DEV void compact_words(WordFn word, int lo, int hi, int pad, int32_t* out, in
 // group compacts the union (ascending ids, device count, padded): no
 // contended atomics.  Threshold mode keeps logit (+ bias) > thr.
 constexpr int kWarpCand = kMaxCand / kTopkWarps;  // per-warp candidate capacity
-constexpr int kStageVec = kTopkSmemCols / 4 / kTopkThreads;  // float4 per thread when staging
+constexpr int kStageVec = 4;  // float4 per thread per staging batch (loads issued together)
+constexpr int kRegCols = 16384;  // rows up to this width stay in registers while the bracket is computed
+constexpr int kRegVec = kRegCols / 4 / kTopkThreads;  // 8 float4 per thread
 
 __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -283,103 +286,138 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   if (!threshold) {
     if (tid == 0) { s_na = 0; s_ovf = 0; s_n2 = 0; }
     for (int i = tid; i < 4096; i += kTopkThreads) hist[i] = 0;
-    // ---- stage the keys (all loads issued first), keep a strided sample
     const int S = min(cols, kSample);
     const int stride = cols / S;
-    if (staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0 &&
-        (!bias || ((uintptr_t)bias & 15) == 0)) {
-      const float4* x4 = reinterpret_cast<const float4*>(x);
-      const float4* b4 = reinterpret_cast<const float4*>(bias);
-      const int n4 = cols >> 2;
-      float4 v[kStageVec], bb[kStageVec];
-#pragma unroll
-      for (int j = 0; j < kStageVec; ++j) {
-        const int i = j * kTopkThreads + tid;
-        if (i < n4) {
-          v[j] = __ldg(x4 + i);
-          if (bias) bb[j] = __ldg(b4 + i);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kStageVec; ++j) {
-        const int i = j * kTopkThreads + tid;
-        if (i < n4) {
-          if (bias) {
-            v[j].x += bb[j].x; v[j].y += bb[j].y; v[j].z += bb[j].z; v[j].w += bb[j].w;
-          }
-          const uint4 u = make_uint4(order_key(v[j].x), order_key(v[j].y), order_key(v[j].z), order_key(v[j].w));
-          *reinterpret_cast<uint4*>(keys + 4 * i) = u;
-          const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int e = 4 * i + t;
-            if (e % stride == 0 && e / stride < S) samp[e / stride] = uu[t];
-          }
-        }
-      }
-    } else {
-      if (staged)
-        for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(logit(i));
-      for (int j = tid; j < S; j += kTopkThreads) samp[j] = order_key(logit(j * stride));
-    }
-    __syncthreads();
-    TK_STAMP(1);
-    // ---- 1. bracket: sample order statistics at 22-bit precision
+    const bool vec_ok = staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0 &&
+                        (!bias || ((uintptr_t)bias & 15) == 0);
     const float q = (float)p.k / (float)cols;
     const float rs = q * (float)S;
     const float dl = 3.f * sqrtf(fmaxf(rs * (1.f - q), 0.f)) + 2.f;
     const bool open_top = rs - dl < 1.f, open_bottom = rs + dl > (float)S;
     const int r_hi = max(1, min(S, (int)floorf(rs - dl)));
     const int r_lo = max(1, min(S, (int)ceilf(rs + dl)));
-    for (int base = 0; base < S; base += kTopkThreads) {
-      const int j = base + tid;
-      const uint32_t u = j < S ? samp[j] : 0u;
-      hist_add_agg(hist, j < S, u >> 20, lane);
-    }
-    __syncthreads();
-    select_bin2<kTopkThreads>(hist, 4096, r_hi, r_lo, s_warp, s_sel);
-    const int bin_hi = s_sel[0], rem_hi = s_sel[1], bin_lo = s_sel[3], rem_lo = s_sel[4];
-    for (int i = tid; i < 2048; i += kTopkThreads) hist[i] = 0;
-    __syncthreads();
-    for (int base = 0; base < S; base += kTopkThreads) {
-      const int j = base + tid;
-      const uint32_t u = j < S ? samp[j] : 0u;
-      const int top = (int)(u >> 20);
-      const uint32_t sub = (u >> 10) & 1023u;
-      hist_add_agg(hist, j < S && top == bin_hi, sub, lane);
-      hist_add_agg(hist + 1024, j < S && top == bin_lo, sub, lane);
-    }
-    __syncthreads();
-    select_bin<kTopkThreads>(hist, 1024, rem_hi, s_warp, s_sel);
-    const uint32_t hi22 = open_top ? 0x3FFFFFu : (((uint32_t)bin_hi << 10) | (uint32_t)s_sel[0]);
-    select_bin<kTopkThreads>(hist + 1024, 1024, rem_lo, s_warp, s_sel);
-    const uint32_t lo22 = open_bottom ? 0u : (((uint32_t)bin_lo << 10) | (uint32_t)s_sel[0]);
-    TK_STAMP(2);
-    // ---- 2. count above / collect candidates into per-warp lists
-    {
-      int n_above = 0, wn = 0;
-      uint32_t* wk = wc_key + warp * kWarpCand;
-      int* wi = wc_idx + warp * kWarpCand;
+    // bracket (22-bit sample order statistics at ranks r_hi / r_lo) from samp[0, S)
+    auto bracket = [&](uint32_t& hi22, uint32_t& lo22) {
+      for (int base = 0; base < S; base += kTopkThreads) {
+        const int j = base + tid;
+        const uint32_t u = j < S ? samp[j] : 0u;
+        hist_add_agg(hist, j < S, u >> 20, lane);
+      }
+      __syncthreads();
+      select_bin2<kTopkThreads>(hist, 4096, r_hi, r_lo, s_warp, s_sel);
+      const int bin_hi = s_sel[0], rem_hi = s_sel[1], bin_lo = s_sel[3], rem_lo = s_sel[4];
+      for (int i = tid; i < 2048; i += kTopkThreads) hist[i] = 0;
+      __syncthreads();
+      for (int base = 0; base < S; base += kTopkThreads) {
+        const int j = base + tid;
+        const uint32_t u = j < S ? samp[j] : 0u;
+        const int top = (int)(u >> 20);
+        const uint32_t sub = (u >> 10) & 1023u;
+        hist_add_agg(hist, j < S && top == bin_hi, sub, lane);
+        hist_add_agg(hist + 1024, j < S && top == bin_lo, sub, lane);
+      }
+      __syncthreads();
+      select_bin<kTopkThreads>(hist, 1024, rem_hi, s_warp, s_sel);
+      hi22 = open_top ? 0x3FFFFFu : (((uint32_t)bin_hi << 10) | (uint32_t)s_sel[0]);
+      select_bin<kTopkThreads>(hist + 1024, 1024, rem_lo, s_warp, s_sel);
+      lo22 = open_bottom ? 0u : (((uint32_t)bin_lo << 10) | (uint32_t)s_sel[0]);
+    };
+    int n_above_t = 0, wn = 0;  // this thread's count above the bracket; this warp's candidates
+    uint32_t* wk = wc_key + warp * kWarpCand;
+    int* wi = wc_idx + warp * kWarpCand;
+    auto classify_key = [&](bool ok, uint32_t u, int i, uint32_t hi22, uint32_t lo22) {
+      const uint32_t t22 = u >> 10;
+      n_above_t += (ok && t22 > hi22) ? 1 : 0;
+      const bool cand = ok && t22 >= lo22 && t22 <= hi22;
+      const uint32_t bal = __ballot_sync(0xffffffffu, cand);
+      const int slot = wn + __popc(bal & ((1u << lane) - 1u));
+      if (cand && slot < kWarpCand) {
+        wk[slot] = u;
+        wi[slot] = i;
+      }
+      wn += __popc(bal);
+    };
+    uint32_t hi22, lo22;
+    if (vec_ok && cols <= kRegCols) {
+      // ---- fused: the row's loads are in flight (registers) while the
+      //      bracket is computed from a strided sample read directly from
+      //      memory; then ONE pass converts, stages and classifies every key
+      const float4* x4 = reinterpret_cast<const float4*>(x);
+      const float4* b4 = reinterpret_cast<const float4*>(bias);
+      const int n4 = cols >> 2;
+      float4 v[kRegVec];
+#pragma unroll
+      for (int j = 0; j < kRegVec; ++j) {
+        const int i = j * kTopkThreads + tid;
+        if (i < n4) v[j] = __ldg(x4 + i);
+      }
+      for (int j = tid; j < S; j += kTopkThreads) samp[j] = order_key(logit(j * stride));
+      __syncthreads();
+      TK_STAMP(1);
+      bracket(hi22, lo22);
+      TK_STAMP(2);
+#pragma unroll
+      for (int j = 0; j < kRegVec; ++j) {
+        const int i = j * kTopkThreads + tid;
+        const bool ok = i < n4;
+        if (ok && bias) {
+          const float4 bb = __ldg(b4 + i);
+          v[j].x += bb.x; v[j].y += bb.y; v[j].z += bb.z; v[j].w += bb.w;
+        }
+        const uint4 u = ok ? make_uint4(order_key(v[j].x), order_key(v[j].y), order_key(v[j].z), order_key(v[j].w))
+                           : make_uint4(0, 0, 0, 0);
+        if (ok) *reinterpret_cast<uint4*>(keys + 4 * i) = u;
+        classify_key(ok, u.x, 4 * i, hi22, lo22);
+        classify_key(ok, u.y, 4 * i + 1, hi22, lo22);
+        classify_key(ok, u.z, 4 * i + 2, hi22, lo22);
+        classify_key(ok, u.w, 4 * i + 3, hi22, lo22);
+      }
+    } else {
+      // ---- stage the keys, keep a strided sample, then bracket and classify
+      if (vec_ok) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* b4 = reinterpret_cast<const float4*>(bias);
+        const int n4 = cols >> 2;
+        for (int i0 = 0; i0 < n4; i0 += kStageVec * kTopkThreads) {
+          float4 v[kStageVec], bb[kStageVec];
+#pragma unroll
+          for (int j = 0; j < kStageVec; ++j) {
+            const int i = i0 + j * kTopkThreads + tid;
+            if (i < n4) {
+              v[j] = __ldg(x4 + i);
+              if (bias) bb[j] = __ldg(b4 + i);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kStageVec; ++j) {
+            const int i = i0 + j * kTopkThreads + tid;
+            if (i < n4) {
+              if (bias) {
+                v[j].x += bb[j].x; v[j].y += bb[j].y; v[j].z += bb[j].z; v[j].w += bb[j].w;
+              }
+              *reinterpret_cast<uint4*>(keys + 4 * i) =
+                  make_uint4(order_key(v[j].x), order_key(v[j].y), order_key(v[j].z), order_key(v[j].w));
+            }
+          }
+        }
+      } else if (staged) {
+        for (int i = tid; i < cols; i += kTopkThreads) keys[i] = order_key(logit(i));
+      }
+      for (int j = tid; j < S; j += kTopkThreads) samp[j] = staged ? keys[j * stride] : order_key(logit(j * stride));
+      __syncthreads();
+      TK_STAMP(1);
+      bracket(hi22, lo22);
+      TK_STAMP(2);
       for (int base = 0; base < cols; base += kTopkThreads) {
         const int i = base + tid;
-        const uint32_t u = i < cols ? key_at(i) : 0u;
-        const uint32_t t22 = u >> 10;
-        const bool above = i < cols && t22 > hi22;
-        const bool cand = i < cols && t22 >= lo22 && t22 <= hi22;
-        n_above += __popc(__ballot_sync(0xffffffffu, above));
-        const uint32_t bal = __ballot_sync(0xffffffffu, cand);
-        const int slot = wn + __popc(bal & ((1u << lane) - 1u));
-        if (cand && slot < kWarpCand) {
-          wk[slot] = u;
-          wi[slot] = i;
-        }
-        wn += __popc(bal);
+        classify_key(i < cols, i < cols ? key_at(i) : 0u, i, hi22, lo22);
       }
-      if (lane == 0) {
-        s_wn[warp] = wn;
-        atomicAdd(&s_na, n_above);
-        if (wn > kWarpCand) s_ovf = 1;
-      }
+    }
+    n_above_t = warp_sum(n_above_t);
+    if (lane == 0) {
+      s_wn[warp] = wn;
+      atomicAdd(&s_na, n_above_t);
+      if (wn > kWarpCand) s_ovf = 1;
     }
     __syncthreads();
     int n_cand = 0, my_off = 0;
@@ -450,7 +488,34 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
 
   // ---- 4. selection
   const int words = (cols + 31) >> 5;
-  if (fast && !p.idx_out) {
+  if (fast && !p.idx_out && !threshold && staged) {
+    // one word per thread: its 32 keys as 8 x 16-byte shared loads, the bit
+    // decisions made locally, the words stored coalesced
+    for (int w = tid; w < words; w += kTopkThreads) {
+      uint32_t bt = 0;
+      const int e0 = w << 5;
+      if (e0 + 32 <= cols) {
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const uint4 u4 = *reinterpret_cast<const uint4*>(keys + e0 + 4 * c4);
+          const uint32_t uu[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+          for (int t2 = 0; t2 < 4; ++t2) {
+            const int e = e0 + 4 * c4 + t2;
+            const bool take = uu[t2] > prefix || (uu[t2] == prefix && e < tie_lim);
+            bt |= (take ? 1u : 0u) << (4 * c4 + t2);
+          }
+        }
+      } else {
+        for (int e = e0; e < cols; ++e) {
+          const uint32_t u = keys[e];
+          bt |= ((u > prefix || (u == prefix && e < tie_lim)) ? 1u : 0u) << (e - e0);
+        }
+      }
+      if (p.row_bits) p.row_bits[(size_t)row * words + w] = bt;
+      else if (p.bitmap && bt) atomicOr(p.bitmap + w, bt);
+    }
+  } else if (fast && !p.idx_out) {
     // decide, ballot, store / OR the word
     for (int w = warp; w < words; w += kTopkWarps) {
       const int e = (w << 5) + lane;
@@ -522,10 +587,97 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   }
   TK_STAMP(5);
 
-  // ---- fused union: group OR by the last CTA of each row group, then the
-  //      last group compacts
+  // ---- fused union
   if (p.row_bits) {
     const int groups = (p.rows + kGroupRows - 1) / kGroupRows;
+    if (p.coresident) {
+      // every row CTA is resident (rows <= SMs, one CTA per SM): a grid
+      // barrier, then CTA c ORs words [w0, w1) over all rows, a second
+      // barrier publishes the per-CTA popcounts, and each CTA writes its
+      // ascending ids at its prefix -- no single-CTA tail
+      int* bar_count = p.tickets + groups + 1;
+      int* bar_gen = p.tickets + groups + 2;
+      int* totals = p.tickets + groups + 3;
+      auto grid_barrier = [&]() {
+        __syncthreads();
+        if (tid == 0) {
+          const int g = *reinterpret_cast<volatile int*>(bar_gen);
+          __threadfence();
+          if (atomicAdd(bar_count, 1) == p.rows - 1) {
+            *bar_count = 0;
+            __threadfence();
+            atomicExch(bar_gen, g + 1);
+          } else {
+            while (*reinterpret_cast<volatile int*>(bar_gen) == g) {
+            }
+          }
+          __threadfence();
+        }
+        __syncthreads();
+      };
+      grid_barrier();
+      TK_STAMP(6);
+      const int wlo = p.lo >> 5, whi = (p.hi + 31) >> 5;
+      const int nw = whi - wlo;
+      const int w0 = wlo + (int)((long long)row * nw / p.rows), w1 = wlo + (int)((long long)(row + 1) * nw / p.rows);
+      const int mine = w1 - w0;  // words of this CTA (<= kTopkThreads for rows >= 1... capped below)
+      // thread -> (word, row slice): all loads in flight at once
+      uint32_t acc = 0;
+      int pw = 1;  // threads per word: a power of two so word groups align with warps
+      while (mine > 0 && pw * 2 * mine <= kTopkThreads) pw *= 2;
+      const int wi = tid / pw, rs = tid - wi * pw;
+      const bool has_word = mine > 0 && wi < mine;
+      if (has_word)
+        for (int r = rs; r < p.rows; r += pw) acc |= __ldcg(p.row_bits + (size_t)r * words + w0 + wi);
+      for (int o = 1; o < pw && o < 32; o <<= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+      __shared__ uint32_t s_or[kTopkWarps];
+      if (pw > 32) {  // a word spans pw/32 warps
+        if (lane == 0) s_or[warp] = acc;
+        __syncthreads();
+        if (rs == 0)
+          for (int q2 = 1; q2 < pw / 32; ++q2) acc |= s_or[warp + q2];
+      }
+      // stage my words' bits (clipped to [lo, hi)) in shared memory (index = word - w0)
+      uint32_t* s_bits = reinterpret_cast<uint32_t*>(cand_key);  // free by now, >= kMaxCand words
+      if (has_word && rs == 0) {
+        const int top = p.hi - ((w0 + wi) << 5);
+        if (top < 32) acc &= (top <= 0) ? 0u : ((1u << top) - 1u);
+        s_bits[wi] = acc;
+      }
+      __syncthreads();
+      // popcount prefix inside the CTA (thread t <-> word t)
+      const uint32_t bits_t = tid < mine ? s_bits[tid] : 0u;
+      int cta_total;
+      const int pos_local = block_excl_scan<kTopkThreads>(__popc(bits_t), s_warp, &cta_total);
+      if (tid == 0) totals[row] = cta_total;
+      grid_barrier();
+      // every CTA's total in one parallel load; prefix over CTAs < row
+      const int tc = tid < p.rows ? __ldcg(totals + tid) : 0;
+      int total;
+      const int excl = block_excl_scan<kTopkThreads>(tc, s_warp, &total);
+      if (tid == row) s_sel[0] = excl;  // rows <= SMs < kTopkThreads
+      __syncthreads();
+      const int before = s_sel[0];
+      uint32_t bits = bits_t;
+      int pos = before + pos_local;
+      while (bits) {
+        const int b2 = __ffs(bits) - 1;
+        bits &= bits - 1;
+        p.union_out[pos++] = ((w0 + tid) << 5) + b2 - p.lo;
+      }
+      if (row == 0 && tid == 0) *p.count_out = total;
+      // the CTA holding the last id pads idx_out up to a multiple of pad
+      if (p.pad > 1 && total > 0 && before < total && before + cta_total >= total) {
+        __syncthreads();
+        const int padded = (total + p.pad - 1) / p.pad * p.pad;
+        const int32_t last = p.union_out[total - 1];
+        for (int i = total + tid; i < padded; i += kTopkThreads) p.union_out[i] = last;
+      }
+      TK_STAMP(7);
+      return;
+    }
+    // rows > SMs: the last CTA of each group of 16 rows ORs the group, and
+    // the last group compacts
     const int g = row / kGroupRows;
     const int g_rows = min(kGroupRows, p.rows - g * kGroupRows);
     __threadfence();
@@ -801,7 +953,7 @@ static size_t su_groups(int rows) { return (size_t)(rows + kGroupRows - 1) / kGr
 
 extern "C" size_t ps_select_union_workspace_bytes(int rows, int cols) {
   if (rows < 1 || cols < 1) return 0;
-  const size_t tickets = (su_groups(rows) + 1) * 4;
+  const size_t tickets = (su_groups(rows) + 3 + (size_t)rows) * 4;
   const size_t head = (tickets + 255) / 256 * 256;
   return head + (su_groups(rows) + (size_t)rows) * su_words(cols) * 4;
 }
@@ -817,9 +969,12 @@ extern "C" int ps_select_union(const float* logits, const float* bias, int rows,
   TopkParams prm{};
   prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k > 0 ? k : 0; prm.thr = thr;
   prm.bias = bias;
-  const size_t tickets = (su_groups(rows) + 1) * 4;
+  const size_t tickets = (su_groups(rows) + 3 + (size_t)rows) * 4;
   const size_t head = (tickets + 255) / 256 * 256;
   uint8_t* base = static_cast<uint8_t*>(ws);
+  // one CTA per row and per SM (the kernel's shared memory): all resident
+  // at once iff rows <= SMs, and every CTA owns <= 512 words
+  prm.coresident = rows <= ps_num_sms() && rows <= kTopkThreads && (cols + 31) / 32 <= (size_t)rows * kTopkThreads;
   prm.tickets = reinterpret_cast<int*>(base);
   prm.group_bits = reinterpret_cast<uint32_t*>(base + head);
   prm.row_bits = prm.group_bits + su_groups(rows) * su_words(cols);

@@ -7,7 +7,7 @@ from paper_2505_14884_b200 import _lib  # noqa: E402
 
 dev = torch.device("cuda")
 L = _lib.load()
-names = ["start", "staged", "bracket", "counted", "kth", "selected", "union", "-", "-", "-"]
+names = ["start", "loaded", "bracket", "counted", "kth", "selected", "barrier1", "union", "-", "-"]
 for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"), (256, 16384, 8192, "hot")]:
     g = torch.Generator(device=dev); g.manual_seed(0)
     lg = torch.randn(rows, cols, device=dev, generator=g)
@@ -32,7 +32,7 @@ for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"),
     t = tr.view(-1, 16).cpu().numpy()
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
-    print(f"== {rows}x{cols} k={k} {dist}: CTAs={len(t)}  span={(t[:, 5].max() - t0) / 1e3:.1f} us  "
+    print(f"== {rows}x{cols} k={k} {dist}: CTAs={len(t)}  span={(max(t[:, 5].max(), t[:, 7].max()) - t0) / 1e3:.1f} us  "
           f"fallbacks={int((t[:, 11] == 1).sum())}  cand(med)={int(np.median(t[:, 10] >> 32))} "
           f"eq(max)={int((t[:, 10] & 0xffffffff).max())}")
     for j in range(1, 10):
