@@ -148,6 +148,14 @@ int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, int pad,
 int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const float* bias,
                         int B, int d, int H_kv, int k,
                         float* logits_out, int32_t* sel_out, void* stream);
+/* Same, fused with the step's KV append (ps_kv_append semantics: k_new /
+ * v_new rows of H_cache heads written at lengths[b], then lengths[b]++; a
+ * full sequence sets err_flag) -- one launch instead of two per layer. */
+int ps_head_router_topk_append(const void* x, int64_t x_ld, const void* w_t, const float* bias,
+                               int B, int d, int H_kv, int k, float* logits_out, int32_t* sel_out,
+                               void* k_cache, void* v_cache, int32_t* lengths,
+                               const void* k_new, const void* v_new, int64_t src_ld,
+                               int H_cache, int cap, int d_h, int32_t* err_flag, void* stream);
 
 /* ======================================================================
  * Gathered GEMM on tcgen05 tensor cores (TMEM accumulators).

@@ -801,10 +801,26 @@ constexpr int kHrWarps = kHrThreads / 32;
 constexpr int kHrMaxHeads = 256;
 constexpr int kHrMaxRows = 4;
 
+// Optional fused KV append (ps_head_router_topk_append): the cluster of row
+// group r0.. also writes the step's K/V rows (tensors.py:150-170) -- CTA j
+// copies cache heads [j*hb, (j+1)*hb) -- and CTA 0 bumps lengths after the
+// cluster barrier, saving the separate append launch.
+struct AppendArgs {
+  uint16_t* kc;
+  uint16_t* vc;
+  int32_t* lengths;
+  const uint16_t* kn;
+  const uint16_t* vn;
+  int64_t src_ld;
+  int Hc, cap, d_h;
+  int32_t* err;
+};
+
 template <int R>
 __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
     const uint16_t* __restrict__ x, int64_t x_ld, const uint16_t* __restrict__ w_t, const float* __restrict__ bias,
-    int B, int d, int H, int HB, int k, float* __restrict__ logits_out, int32_t* __restrict__ sel_out) {
+    int B, int d, int H, int HB, int k, float* __restrict__ logits_out, int32_t* __restrict__ sel_out,
+    const AppendArgs ap) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ float s_log[kHrMaxRows * kHrMaxHeads];          // CTA 0: the cluster's logits
   __shared__ float s_part[kHrWarps * 2][kHrMaxRows];         // per-item partial sums
@@ -823,6 +839,28 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r < nr) v = *reinterpret_cast<const uint4*>(x + (size_t)(r0 + r) * x_ld + cc * 8);
     *reinterpret_cast<uint4*>(sx + r * d + cc * 8) = v;
+  }
+  if (ap.kc) {
+    const int hb = (ap.Hc + csize - 1) / csize, ha0 = crank * hb, ha1 = min(ap.Hc, ha0 + hb);
+    const int vph = ap.d_h >> 3;
+    for (int r = 0; r < nr; ++r) {
+      const int b = r0 + r;
+      const int pos = ap.lengths[b];
+      if (pos >= ap.cap) {
+        if (tid == 0 && crank == 0 && ap.err) *ap.err = 1;
+        continue;
+      }
+      const int total = max(0, ha1 - ha0) * vph;
+      for (int e = tid; e < total; e += kHrThreads) {
+        const int h = ha0 + e / vph, c = e - (e / vph) * vph;
+        const size_t src = (size_t)b * ap.src_ld + (size_t)h * ap.d_h + c * 8;
+        const size_t dst = (((size_t)b * ap.Hc + h) * ap.cap + pos) * ap.d_h + c * 8;
+        const uint4 kv = __ldg(reinterpret_cast<const uint4*>(ap.kn + src));
+        const uint4 vv = __ldg(reinterpret_cast<const uint4*>(ap.vn + src));
+        *reinterpret_cast<uint4*>(ap.kc + dst) = kv;
+        *reinterpret_cast<uint4*>(ap.vc + dst) = vv;
+      }
+    }
   }
   const int h0 = crank * HB;
   const int hn = max(0, min(HB, H - h0));
@@ -880,6 +918,8 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
   }
   cluster_sync_all();
   if (crank != 0) return;
+  // every CTA of the cluster read lengths[] before the barrier: bump them now
+  if (ap.kc && tid < nr && ap.lengths[r0 + tid] < ap.cap) ap.lengths[r0 + tid] += 1;
   // top-k of each row by rank counting, one warp per row
   if (warp < nr) {
     const int r = warp;
@@ -908,7 +948,7 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
 
 template <int R>
 int launch_head_router(const uint16_t* x, int64_t x_ld, const uint16_t* w_t, const float* bias, int B, int d,
-                       int H, int k, float* logits_out, int32_t* sel_out, cudaStream_t st) {
+                       int H, int k, float* logits_out, int32_t* sel_out, const AppendArgs& ap, cudaStream_t st) {
   auto kern = head_router_topk_kernel<R>;
   const size_t smem = (size_t)R * d * 2;
   static bool configured = false;
@@ -921,7 +961,7 @@ int launch_head_router(const uint16_t* x, int64_t x_ld, const uint16_t* w_t, con
   const int HB = (H + csize - 1) / csize;
   const int groups = (B + R - 1) / R;
   return launch_ex(kern, dim3(groups * csize), dim3(kHrThreads), smem, st, csize, x, x_ld, w_t, bias, B, d, H, HB, k,
-                   logits_out, sel_out);
+                   logits_out, sel_out, ap);
 }
 
 }  // namespace
@@ -1002,8 +1042,8 @@ extern "C" int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, in
                    bitmap, width, lo, hi, pad, idx_out, count_out);
 }
 
-extern "C" int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const float* bias, int B, int d,
-                                   int H_kv, int k, float* logits_out, int32_t* sel_out, void* stream) {
+static int head_router_common(const void* x, int64_t x_ld, const void* w_t, const float* bias, int B, int d, int H_kv,
+                              int k, float* logits_out, int32_t* sel_out, const AppendArgs& ap, void* stream) {
   if (B < 1 || d < 8 || d % 8 || H_kv < 1 || H_kv > kHrMaxHeads || k < 1 || k > H_kv) return PS_ERR_VALUE;
   if (!x || !w_t || !sel_out || x_ld < d || x_ld % 8) return PS_ERR_VALUE;
   if ((size_t)kHrMaxRows * d * 2 > 160 * 1024) return PS_ERR_UNSUPPORTED;
@@ -1011,7 +1051,29 @@ extern "C" int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t,
   const auto* wp = static_cast<const uint16_t*>(w_t);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // rows per cluster: keep >= ~64 clusters in flight, fewer W^T re-reads at large batch
-  if (B >= 256) return launch_head_router<4>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, st);
-  if (B >= 128) return launch_head_router<2>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, st);
-  return launch_head_router<1>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, st);
+  if (B >= 256) return launch_head_router<4>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, ap, st);
+  if (B >= 128) return launch_head_router<2>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, ap, st);
+  return launch_head_router<1>(xp, x_ld, wp, bias, B, d, H_kv, k, logits_out, sel_out, ap, st);
+}
+
+extern "C" int ps_head_router_topk(const void* x, int64_t x_ld, const void* w_t, const float* bias, int B, int d,
+                                   int H_kv, int k, float* logits_out, int32_t* sel_out, void* stream) {
+  AppendArgs ap{};
+  return head_router_common(x, x_ld, w_t, bias, B, d, H_kv, k, logits_out, sel_out, ap, stream);
+}
+
+extern "C" int ps_head_router_topk_append(const void* x, int64_t x_ld, const void* w_t, const float* bias, int B,
+                                          int d, int H_kv, int k, float* logits_out, int32_t* sel_out,
+                                          void* k_cache, void* v_cache, int32_t* lengths, const void* k_new,
+                                          const void* v_new, int64_t src_ld, int H_cache, int cap, int d_h,
+                                          int32_t* err_flag, void* stream) {
+  if (!k_cache || !v_cache || !lengths || !k_new || !v_new || H_cache < 1 || cap < 1 || d_h < 8 || d_h % 8 ||
+      src_ld < (int64_t)H_cache * d_h || src_ld % 8)
+    return PS_ERR_VALUE;
+  if (((uintptr_t)k_new % 16) || ((uintptr_t)v_new % 16) || ((uintptr_t)k_cache % 16) || ((uintptr_t)v_cache % 16))
+    return PS_ERR_VALUE;
+  AppendArgs ap{static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths,
+                static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), src_ld, H_cache, cap, d_h,
+                err_flag};
+  return head_router_common(x, x_ld, w_t, bias, B, d, H_kv, k, logits_out, sel_out, ap, stream);
 }

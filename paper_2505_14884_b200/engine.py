@@ -294,11 +294,12 @@ class DecodeEngine:
             n += self._linear_bf16(self.h, lw.w_qkv_t, lw.b_qkv, self.qkv, tag="gg_qkv")
             kq = self.qkv[:, self.d_loc:]
             vq = self.qkv[:, self.d_loc + self.dk_loc:]
-            _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths), _lib.ptr(kq),
-                                      _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity, cfg.head_dim,
-                                      _lib.ptr(c._err), st), "ps_kv_append")
-            n += 1
             k_h = self.k_heads[ell]
+            if not k_h:
+                _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths), _lib.ptr(kq),
+                                          _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity, cfg.head_dim,
+                                          _lib.ptr(c._err), st), "ps_kv_append")
+                n += 1
             if k_h:
                 sel = self.sel[:, :k_h]
                 if k_h != self.sel.shape[1]:
@@ -306,7 +307,8 @@ class DecodeEngine:
                 hl = None
                 if self.record is not None:
                     hl = torch.empty(B, cfg.kv_heads, dtype=torch.float32, device=self.device)
-                self.head_routers[ell].select_into(self.h, k_h, sel, hl)
+                # head router + top-k fused with the KV append (one launch)
+                self.head_routers[ell].select_append_into(self.h, k_h, sel, c, kq, vq, qkv_w, hl)
                 n += 1
                 if self.record is not None:
                     self.record.setdefault("head_logits", []).append(hl)

@@ -72,6 +72,16 @@ class HeadRouter:
         _lib.call("ps_head_router_topk", _lib.ptr(x2d), x2d.stride(0), _lib.ptr(self.w_t), _lib.ptr(self.b),
                   B, d, self.n_heads, int(k), _lib.ptr(logits_out), _lib.ptr(sel_out), _lib.stream_ptr())
 
+    def select_append_into(self, x2d: torch.Tensor, k: int, sel_out: torch.Tensor, cache, k_new, v_new,
+                           src_ld: int, logits_out=None) -> None:
+        """select_into fused with the step's KV append into ``cache``
+        (tensors.py:150-170 semantics; one launch instead of two)."""
+        B, d = x2d.shape
+        _lib.call("ps_head_router_topk_append", _lib.ptr(x2d), x2d.stride(0), _lib.ptr(self.w_t), _lib.ptr(self.b),
+                  B, d, self.n_heads, int(k), _lib.ptr(logits_out), _lib.ptr(sel_out), _lib.ptr(cache.keys),
+                  _lib.ptr(cache.values), _lib.ptr(cache.lengths), _lib.ptr(k_new), _lib.ptr(v_new), int(src_ld),
+                  cache.kv_heads, cache.capacity, cache.head_dim, _lib.ptr(cache._err), _lib.stream_ptr())
+
     def decision_function(self, x) -> torch.Tensor:
         """routers.py:178-186: per-head logits (f32), vector or batch."""
         xb, single = _as_batch(x, self.d_model, self.w_t.device)

@@ -309,6 +309,34 @@ def test_attention_tensor_core_path_poison_and_agreement(H, H_kv):
     assert (core - clean).abs().max().item() <= 1e-2
 
 
+def test_head_router_fused_append_matches_separate_ops():
+    """ps_head_router_topk_append == ps_kv_append + ps_head_router_topk."""
+    rng = np.random.default_rng(9)
+    for B, d, H_kv, d_h in [(8, 256, 8, 32), (130, 512, 4, 128), (300, 256, 8, 64)]:
+        hr = pb.HeadRouter(d, H_kv, seed=3, device=DEV)
+        x = t(po.round_bf16(rng.normal(size=(B, d)).astype(np.float32)), torch.bfloat16)
+        kv = t(rng.normal(size=(B, 2 * H_kv * d_h)).astype(np.float32), torch.bfloat16)
+        kq, vq = kv[:, :H_kv * d_h], kv[:, H_kv * d_h:]
+        caches = []
+        for _ in range(2):
+            c = pb.KVCache(B, H_kv, 20, d_h, device=DEV)
+            c.set_lengths(rng.integers(0, 20, size=B) if not caches else caches[0].host_lengths)
+            caches.append(c)
+        caches[1].set_lengths(caches[0].host_lengths)
+        caches[0].set_lengths(np.minimum(caches[0].host_lengths, 19))
+        caches[1].set_lengths(caches[0].host_lengths)
+        k = max(1, H_kv // 2)
+        s1 = torch.zeros(B, k, dtype=torch.int32, device=DEV)
+        s2 = torch.zeros_like(s1)
+        caches[0].append_step(kq.reshape(B, H_kv, d_h), vq.reshape(B, H_kv, d_h))
+        hr.select_into(x, k, s1)
+        hr.select_append_into(x, k, s2, caches[1], kq, vq, kv.stride(0))
+        torch.cuda.synchronize()
+        assert torch.equal(s1, s2)
+        assert torch.equal(caches[0].lengths, caches[1].lengths)
+        assert torch.equal(caches[0].keys, caches[1].keys) and torch.equal(caches[0].values, caches[1].values)
+
+
 # ----------------------------------------------------------------- MLP / GEMM
 
 def test_mlp_matches_reference(golden):
