@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--kv-ring", type=int, default=0, help="alias KV storage over this many buffers (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
-    ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native"])
+    ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
     return ap.parse_args()
 
 

@@ -309,6 +309,13 @@ PS_DEV uint32_t map_peer(uint32_t saddr, uint32_t rank) {
 PS_DEV void st_dsmem_f32(uint32_t addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
+// asynchronous remote store that signals `bytes` on the remote CTA's mbarrier
+// (complete_tx): a producer->consumer DSMEM hand-off without cluster fences
+PS_DEV void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr),
+               "r"(__float_as_uint(v)), "r"(remote_bar)
+               : "memory");
+}
 PS_DEV void red_dsmem_add_u32(uint32_t addr, uint32_t v) {
   asm volatile("red.shared::cluster.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }

@@ -832,7 +832,13 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
   const int nr = min(R, B - r0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int chunks = d >> 3;
+  // CTA 0's arrival barrier for the cluster's logits (st.async complete_tx);
   // every CTA of the cluster must have started before its DSMEM is written
+  __shared__ uint64_t s_bar;
+  if (crank == 0 && tid == 0) {
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
+  }
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   for (int c = tid; c < R * chunks; c += kHrThreads) {
     const int r = c / chunks, cc = c - r * chunks;
@@ -872,6 +878,8 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   const uint32_t s_log_base = smem_u32(s_log);
   const uint32_t leader_log = map_peer(s_log_base, 0);
+  const uint32_t leader_bar = map_peer(smem_u32(&s_bar), 0);
+  if (crank == 0 && tid == 0) mbar_arrive_expect_tx(&s_bar, (uint32_t)(nr * H * 4));
   for (int it0 = 0; it0 < items; it0 += kHrWarps) {
     const int it = it0 + warp;
     if (it < items) {
@@ -910,15 +918,15 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
           for (int q = 0; q < segs; ++q) v += s_part[j + q][r];  // segments of a head are adjacent slots
           const int h = h0 + hh;
           v += bias ? bias[h] : 0.f;
-          st_dsmem_f32(leader_log + (uint32_t)(r * H + h) * 4u, v);
+          st_async_f32(leader_log + (uint32_t)(r * H + h) * 4u, v, leader_bar);
         }
       }
     }
     __syncthreads();
   }
-  cluster_sync_all();
   if (crank != 0) return;
-  // every CTA of the cluster read lengths[] before the barrier: bump them now
+  mbar_wait(&s_bar, 0);  // every CTA's logits landed (they read lengths[] before sending)
+  // every CTA of the cluster read lengths[] before its logits arrived: bump them now
   if (ap.kc && tid < nr && ap.lengths[r0 + tid] < ap.cap) ap.lengths[r0 + tid] += 1;
   // top-k of each row by rank counting, one warp per row
   if (warp < nr) {

@@ -94,7 +94,7 @@ class DecodeEngine:
         self.dense_backend = check_choice(dense_backend, ("cublas", "native"), "dense_backend")
         # the MLP router's two layers: tcgen05 kernels with their static weights
         # streamed ahead of the previous launch (PDL), or cuBLAS
-        self.router_backend = check_choice(router_backend or dense_backend, ("cublas", "native"),
+        self.router_backend = check_choice(router_backend or dense_backend, ("cublas", "native", "native_in"),
                                            "router_backend")
         self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
@@ -329,8 +329,13 @@ class DecodeEngine:
             if self.sparse_mlp:
                 r = self.mlp_routers[ell]
                 out_bias = None  # the router's output bias is added inside ps_select_union
-                if self.router_backend == "cublas":
-                    n += self._linear_bf16(self.h, r.w_in_t, r.b_in, self.r_hid, act_relu=True)
+                if self.router_backend in ("cublas", "native_in"):
+                    if self.router_backend == "native_in":  # tcgen05 kernel, static weights prefetched (PDL)
+                        gather_gemm_into(r.w_in_t, None, None, self.h, self.h.stride(0), r.b_in, B, r.hidden_dim_,
+                                         d, _lib.PS_ACT_RELU, self.r_hid, self.r_hid.stride(0), tag="gg_router")
+                        n += 1
+                    else:
+                        n += self._linear_bf16(self.h, r.w_in_t, r.b_in, self.r_hid, act_relu=True)
                     torch.mm(self.r_hid, r.w_out_t.t(), out_dtype=torch.float32, out=self.r_logits)
                     out_bias = r.b_out
                 else:
