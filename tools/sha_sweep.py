@@ -17,7 +17,7 @@ if OLD is not None:
     from paper_2505_14884_b200 import _lib  # noqa: E402
     for _n in ("ps_sha_workspace_bytes", "ps_sha_decode"):
         getattr(OLD, _n).restype, getattr(OLD, _n).argtypes = _lib.SIGNATURES[_n]
-for (B, H, H_kv, ctx, ks) in [(64, 32, 32, 1920, (16, 32)), (128, 32, 32, 1920, (16,)), (64, 32, 8, 1920, (4, 8)), (8, 32, 32, 1920, (16,))]:
+for (B, H, H_kv, ctx, ks) in [(256, 32, 8, 1920, (4, 8)), (512, 32, 8, 1920, (4,)), (64, 32, 32, 1920, (16,))]:
     n = 4
     caches = []
     for i in range(n):
@@ -36,7 +36,7 @@ for (B, H, H_kv, ctx, ks) in [(64, 32, 32, 1920, (16, 32)), (128, 32, 32, 1920, 
             us = timeit(f, 12)
             res.append(f"s={s or 'auto'}:{us:6.1f}us/{nb / us / 1e3:5.0f}")
         print(f"B={B} H_kv={H_kv} k={kh} ctx={ctx}: " + "  ".join(res), flush=True)
-        if OLD is not None:  # the previous (per-unit split) kernel, same process / box
+        if False and OLD is not None:  # the previous (per-unit split) kernel, same process / box
             res = []
             for sp in (1, 2, 3, 4):
                 nbytes = OLD.ps_sha_workspace_bytes(B, H, H_kv, 128, kh, sp)
