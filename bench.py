@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
     ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
+    ap.add_argument("--concurrent-head-router", action="store_true",
+                    help="head router as a concurrent graph branch instead of fused with the KV append")
     return ap.parse_args()
 
 
@@ -303,7 +305,7 @@ def run_ours(args):
     polar = SparsityPolicy(mode="polar", head_density=args.rho,
                            mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
     eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring,
-                       router_backend=args.router_backend)
+                       router_backend=args.router_backend, concurrent_router=args.concurrent_head_router)
     eng.fill_random(ctx, seed=99 + rank)
     dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches)
     tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()

@@ -86,7 +86,8 @@ class DecodeEngine:
 
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
-                 caches=None, dense_backend: str = "cublas", router_backend: str | None = None):
+                 caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
+                 concurrent_router: bool = False):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
@@ -96,6 +97,10 @@ class DecodeEngine:
         # streamed ahead of the previous launch (PDL), or cuBLAS
         self.router_backend = check_choice(router_backend or dense_backend, ("cublas", "native", "native_in"),
                                            "router_backend")
+        # head router on a side stream, concurrent with the QKV GEMM (a
+        # parallel branch of the captured graph); False = fused with the append
+        self.concurrent_router = concurrent_router
+        self.side = torch.cuda.Stream(device=model.device) if concurrent_router else None
         self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
         self.tp = tp
@@ -291,28 +296,30 @@ class DecodeEngine:
             c = self.caches[ell]
             n += self._ln(lw.ln1_g, lw.ln1_b, pending)
             pending = None
+            k_h = self.k_heads[ell]
+            if k_h and self.concurrent_router:
+                # the head router depends only on h1: run it on a side stream
+                # (a parallel graph branch) concurrently with the QKV GEMM
+                main = torch.cuda.current_stream()
+                self.side.wait_stream(main)
+                with torch.cuda.stream(self.side):
+                    sel = self._head_select(ell, k_h)
+                n += 1
             n += self._linear_bf16(self.h, lw.w_qkv_t, lw.b_qkv, self.qkv, tag="gg_qkv")
             kq = self.qkv[:, self.d_loc:]
             vq = self.qkv[:, self.d_loc + self.dk_loc:]
-            k_h = self.k_heads[ell]
-            if not k_h:
+            if not k_h or self.concurrent_router:
+                st = _lib.stream_ptr()
                 _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths), _lib.ptr(kq),
                                           _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity, cfg.head_dim,
                                           _lib.ptr(c._err), st), "ps_kv_append")
                 n += 1
-            if k_h:
-                sel = self.sel[:, :k_h]
-                if k_h != self.sel.shape[1]:
-                    sel = self.sel_bufs(k_h)
-                hl = None
-                if self.record is not None:
-                    hl = torch.empty(B, cfg.kv_heads, dtype=torch.float32, device=self.device)
+            if k_h and self.concurrent_router:
+                torch.cuda.current_stream().wait_stream(self.side)
+            elif k_h:
                 # head router + top-k fused with the KV append (one launch)
-                self.head_routers[ell].select_append_into(self.h, k_h, sel, c, kq, vq, qkv_w, hl)
+                sel = self._head_select(ell, k_h, append=(c, kq, vq, qkv_w))
                 n += 1
-                if self.record is not None:
-                    self.record.setdefault("head_logits", []).append(hl)
-                    self.record.setdefault("heads", []).append(sel.clone())
             else:
                 sel = self.sel_full
             sha_decode_into(self.qkv, qkv_w, c, sel, self.H_loc, self.scale, self.attn, self.d_loc,
@@ -386,6 +393,26 @@ class DecodeEngine:
         n += self._linear_f32(self.h, m.unembed_t, None, self.logits, tag="gg_lm")
         torch.argmax(self.logits, dim=1, out=self.next_tokens)
         return n
+
+    def _head_select(self, ell: int, k_h: int, append=None) -> torch.Tensor:
+        """Head router + per-row top-k into the selection buffer (optionally
+        fused with the KV append)."""
+        B = self.B
+        sel = self.sel[:, :k_h]
+        if k_h != self.sel.shape[1]:
+            sel = self.sel_bufs(k_h)
+        hl = None
+        if self.record is not None:
+            hl = torch.empty(B, self.cfg.kv_heads, dtype=torch.float32, device=self.device)
+        if append is None:
+            self.head_routers[ell].select_into(self.h, k_h, sel, hl)
+        else:
+            c, kq, vq, ld = append
+            self.head_routers[ell].select_append_into(self.h, k_h, sel, c, kq, vq, ld, hl)
+        if self.record is not None:
+            self.record.setdefault("head_logits", []).append(hl)
+            self.record.setdefault("heads", []).append(sel.clone())
+        return sel
 
     def _dense_down(self, mk, hid):
         """x += hid @ W2 with W2^T stored neuron-major (D, d): a plain
