@@ -71,9 +71,24 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(float* __restrict
                                                                uint16_t* __restrict__ y, int64_t y_ld) {
   __shared__ float red[2][kLnThreads / 32];
   float* xr = x + (size_t)blockIdx.x * x_ld;
+  const int n4 = d >> 2;
+  // gamma / beta / pending bias are static: copied to shared memory with
+  // cp.async before the dependency wait (their latency overlaps the
+  // previous kernel's tail)
+  extern __shared__ __align__(16) float ln_smem[];
+  float* sg = ln_smem;
+  float* sb = ln_smem + d;
+  float* sa = ln_smem + 2 * d;
+  for (int i = threadIdx.x; i < n4; i += kLnThreads) {
+    cp_async16(sg + 4 * i, g + 4 * i, 16);
+    cp_async16(sb + 4 * i, bta + 4 * i, 16);
+    if (ADD) cp_async16(sa + 4 * i, add + 4 * i, 16);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   griddep_wait();
   griddep_launch();
-  const int n4 = d >> 2;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
   float4 v[kLnSlots];
   float s = 0.f;
 #pragma unroll
@@ -82,7 +97,7 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(float* __restrict
     if (i < n4) {
       v[j] = *reinterpret_cast<const float4*>(xr + 4 * i);
       if (ADD) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(add) + i);
+        const float4 a = *reinterpret_cast<const float4*>(sa + 4 * i);
         v[j].x += a.x; v[j].y += a.y; v[j].z += a.z; v[j].w += a.w;
         *reinterpret_cast<float4*>(xr + 4 * i) = v[j];
       }
@@ -118,8 +133,8 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(float* __restrict
   for (int j = 0; j < kLnSlots; ++j) {
     const int i = j * kLnThreads + threadIdx.x;
     if (i < n4) {
-      const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + i);
-      const float4 bb = __ldg(reinterpret_cast<const float4*>(bta) + i);
+      const float4 gg = *reinterpret_cast<const float4*>(sg + 4 * i);
+      const float4 bb = *reinterpret_cast<const float4*>(sb + 4 * i);
       uint2 o;
       o.x = pack_bf16x2((v[j].x - mean) * rstd * gg.x + bb.x, (v[j].y - mean) * rstd * gg.y + bb.y);
       o.y = pack_bf16x2((v[j].z - mean) * rstd * gg.z + bb.z, (v[j].w - mean) * rstd * gg.w + bb.w);
@@ -229,7 +244,19 @@ static int ln_launch(float* x, int64_t x_ld, const float* add, const float* gamm
       (add && ((uintptr_t)add % 16)))
     return PS_ERR_VALUE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return launch_ex(add ? layernorm_kernel<true> : layernorm_kernel<false>, dim3(B), dim3(kLnThreads), 0, st, 1, x,
+  const size_t smem = (size_t)(add ? 3 : 2) * d * 4;
+  {
+    static bool big = false;  // opt in once (first call is eager, before any graph capture)
+    if (!big) {
+      if (cudaFuncSetAttribute(layernorm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+              cudaSuccess ||
+          cudaFuncSetAttribute(layernorm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+              cudaSuccess)
+        return PS_ERR_CUDA;
+      big = true;
+    }
+  }
+  return launch_ex(add ? layernorm_kernel<true> : layernorm_kernel<false>, dim3(B), dim3(kLnThreads), smem, st, 1, x,
                    x_ld, add, gamma, beta, d, static_cast<uint16_t*>(y), y_ld);
 }
 

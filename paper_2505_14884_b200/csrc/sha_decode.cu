@@ -824,8 +824,14 @@ int sha_auto_splits(int units, int NT) {
 }
 
 int sha_ctas(int units, int NT, int num_splits) {
-  if (num_splits <= 0) num_splits = sha_auto_splits(units, NT);
-  long long cap = (long long)units * num_splits;
+  // num_splits < 0: exactly -num_splits stream-K CTAs (tuning hook)
+  long long cap;
+  if (num_splits < 0) {
+    cap = -(long long)num_splits;
+  } else {
+    if (num_splits == 0) num_splits = sha_auto_splits(units, NT);
+    cap = (long long)units * num_splits;
+  }
   const long long F = (long long)units * NT;
   if (cap > F) cap = F;
   return (int)(cap < 1 ? 1 : cap);
@@ -844,7 +850,7 @@ using namespace ps;
 extern "C" size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int top_k, int num_splits) {
   if (B < 1 || H_kv < 1 || top_k < 1 || H % H_kv) return 0;
   const size_t units = (size_t)B * top_k;
-  const int n = (int)(units * (num_splits > 0 ? num_splits : 8));  // upper bound of sha_ctas
+  const int n = num_splits < 0 ? -num_splits : (int)(units * (num_splits > 0 ? num_splits : 8));  // >= sha_ctas
   return kCounterBytes + units * (size_t)sha_max_seg((int)units, n) * (size_t)partial_floats(H / H_kv, d_h) * 4;
 }
 
@@ -871,7 +877,6 @@ extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, c
     return PS_ERR_VALUE;
   if (d_h < 8 || d_h > 256 || (d_h & (d_h - 1))) return PS_ERR_UNSUPPORTED;
   const int G = H / H_kv;
-  if (num_splits < 0) num_splits = 0;
   if (ws_bytes < ps_sha_workspace_bytes(B, H, H_kv, d_h, top_k, num_splits)) return PS_ERR_WORKSPACE;
   // max_len_hint must bound every lengths[b]: rows beyond NT tiles are not read
   const int T = kTileBytes / (d_h * 2);

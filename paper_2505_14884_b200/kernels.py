@@ -165,7 +165,7 @@ def sha_decode_into(q2d: torch.Tensor, q_ld: int, cache: KVCache, sel: torch.Ten
     B, H_kv, cap, d_h = cache.keys.shape
     k = sel.shape[1]
     lib = _lib.load()
-    if num_splits <= 0:
+    if num_splits == 0:
         num_splits = lib.ps_sha_auto_splits(B, H_kv, d_h, k, max_len_hint or cap)
     nbytes = lib.ps_sha_workspace_bytes(B, n_heads, H_kv, d_h, k, num_splits)
     ws = _ws.get("sha", nbytes, cache.device)

@@ -23,7 +23,7 @@ from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy  # noqa: E
 from paper_2505_14884_b200.model import DeviceModel, TransformerConfig  # noqa: E402
 
 
-def _engine(kv_heads, mode, record=False):
+def _engine(kv_heads, mode, record=False, **kw):
     cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 288, "relu")
     host = po.random_model(2, 256, 1024, 8, kv_heads, 512, 288, seed=21)
     model = DeviceModel.from_host(cfg, host)
@@ -32,7 +32,7 @@ def _engine(kv_heads, mode, record=False):
                             head_density=0.5 if polar else 1.0)
     hr = [pb.HeadRouter(256, kv_heads, seed=40 + ell) for ell in range(2)]
     mr = [pb.MlpRouter(256, 1024, seed=30 + ell) for ell in range(2)]
-    eng = DecodeEngine(model, 8, 288, policy, head_routers=hr, mlp_routers=mr)
+    eng = DecodeEngine(model, 8, 288, policy, head_routers=hr, mlp_routers=mr, **kw)
     rng = np.random.default_rng(22)  # reference bench.py:70-100 draw order
     for c in eng.caches:
         c.fill_random(rng, 256)
@@ -92,10 +92,12 @@ def test_polar_step_selection_and_logits(golden, tag, kv_heads):
         assert _rel(logits, golden[f"dec_{tag}_polar_logits"]) <= 2e-2
 
 
-@pytest.mark.parametrize("mode", ["dense", "polar"])
-def test_graph_replay_equals_eager(mode):
+@pytest.mark.parametrize("mode,concurrent", [("dense", False), ("polar", False), ("polar", True)])
+def test_graph_replay_equals_eager(mode, concurrent):
+    """Graph replay == eager; with concurrent=True the head router runs on a
+    side stream (a parallel branch of the captured graph)."""
     eng_a, tokens = _engine(8, mode)
-    eng_b, _ = _engine(8, mode)
+    eng_b, _ = _engine(8, mode, concurrent_router=concurrent)
     eng_b.capture()
     for _ in range(3):
         la = eng_a.step(tokens).clone()
