@@ -52,6 +52,7 @@ constexpr int kSample = 2048;         // strided sample of a row that brackets t
 constexpr int kMaxCand = 3072;        // keys inside the bracket kept for the exact select
 constexpr int kGroupRows = 16;        // union: rows ORed by the last CTA of each row group
 constexpr int kMaxGroups = 64;        // ps_select_union: rows <= 1024
+constexpr int kUnionWPT = 4;          // co-resident union: words per thread (cols <= 65536)
 
 struct TopkParams {
   const float* logits;
@@ -617,58 +618,68 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       };
       grid_barrier();
       TK_STAMP(6);
+      // every CTA ORs ALL words over the rows (L2-resident, coalesced) and
+      // scans their popcounts, so it knows the global prefix of its own word
+      // range without a second barrier; it then writes only its range's ids
       const int wlo = p.lo >> 5, whi = (p.hi + 31) >> 5;
       const int nw = whi - wlo;
       const int w0 = wlo + (int)((long long)row * nw / p.rows), w1 = wlo + (int)((long long)(row + 1) * nw / p.rows);
-      const int mine = w1 - w0;  // words of this CTA (<= kTopkThreads for rows >= 1... capped below)
-      // thread -> (word, row slice): all loads in flight at once
-      uint32_t acc = 0;
-      int pw = 1;  // threads per word: a power of two so word groups align with warps
-      while (mine > 0 && pw * 2 * mine <= kTopkThreads) pw *= 2;
-      const int wi = tid / pw, rs = tid - wi * pw;
-      const bool has_word = mine > 0 && wi < mine;
-      if (has_word)
-        for (int r = rs; r < p.rows; r += pw) acc |= __ldcg(p.row_bits + (size_t)r * words + w0 + wi);
-      for (int o = 1; o < pw && o < 32; o <<= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
-      __shared__ uint32_t s_or[kTopkWarps];
-      if (pw > 32) {  // a word spans pw/32 warps
-        if (lane == 0) s_or[warp] = acc;
-        __syncthreads();
-        if (rs == 0)
-          for (int q2 = 1; q2 < pw / 32; ++q2) acc |= s_or[warp + q2];
+      const int kw = (nw + kTopkThreads - 1) / kTopkThreads;  // contiguous words per thread (<= kUnionWPT)
+      const int tw0 = wlo + tid * kw;
+      uint32_t wb[kUnionWPT];
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kUnionWPT; ++j) {
+        const int w = tw0 + j;
+        uint32_t acc = 0;
+        if (j < kw && w < whi) {
+#pragma unroll 8
+          for (int r = 0; r < p.rows; ++r) acc |= __ldcg(p.row_bits + (size_t)r * words + w);
+          const int top = p.hi - (w << 5);
+          if (top < 32) acc &= (top <= 0) ? 0u : ((1u << top) - 1u);
+        }
+        wb[j] = acc;
+        cnt += __popc(acc);
       }
-      // stage my words' bits (clipped to [lo, hi)) in shared memory (index = word - w0)
-      uint32_t* s_bits = reinterpret_cast<uint32_t*>(cand_key);  // free by now, >= kMaxCand words
-      if (has_word && rs == 0) {
-        const int top = p.hi - ((w0 + wi) << 5);
-        if (top < 32) acc &= (top <= 0) ? 0u : ((1u << top) - 1u);
-        s_bits[wi] = acc;
-      }
-      __syncthreads();
-      // popcount prefix inside the CTA (thread t <-> word t)
-      const uint32_t bits_t = tid < mine ? s_bits[tid] : 0u;
-      int cta_total;
-      const int pos_local = block_excl_scan<kTopkThreads>(__popc(bits_t), s_warp, &cta_total);
-      if (tid == 0) totals[row] = cta_total;
-      grid_barrier();
-      // every CTA's total in one parallel load; prefix over CTAs < row
-      const int tc = tid < p.rows ? __ldcg(totals + tid) : 0;
       int total;
-      const int excl = block_excl_scan<kTopkThreads>(tc, s_warp, &total);
-      if (tid == row) s_sel[0] = excl;  // rows <= SMs < kTopkThreads
-      __syncthreads();
-      const int before = s_sel[0];
-      uint32_t bits = bits_t;
-      int pos = before + pos_local;
-      while (bits) {
-        const int b2 = __ffs(bits) - 1;
-        bits &= bits - 1;
-        p.union_out[pos++] = ((w0 + tid) << 5) + b2 - p.lo;
+      int pos = block_excl_scan<kTopkThreads>(cnt, s_warp, &total);
+#pragma unroll
+      for (int j = 0; j < kUnionWPT; ++j) {
+        const int w = tw0 + j;
+        uint32_t bits = wb[j];
+        if (w >= w0 && w < w1) {
+          while (bits) {
+            const int b2 = __ffs(bits) - 1;
+            bits &= bits - 1;
+            p.union_out[pos++] = (w << 5) + b2 - p.lo;
+          }
+        } else {
+          pos += __popc(bits);
+        }
       }
       if (row == 0 && tid == 0) *p.count_out = total;
-      // the CTA holding the last id pads idx_out up to a multiple of pad
-      if (p.pad > 1 && total > 0 && before < total && before + cta_total >= total) {
-        __syncthreads();
+      // the CTA whose range holds the last id pads idx_out up to a multiple of pad
+      __shared__ int s_range[2];
+      if (tid == 0) { s_range[0] = 0x7fffffff; s_range[1] = -1; }
+      __syncthreads();
+      {
+        // global positions covered by this CTA's words
+        int lo_pos = 0x7fffffff, hi_pos = -1, p2 = pos;
+        for (int j = kUnionWPT - 1; j >= 0; --j) {
+          const int w = tw0 + j;
+          p2 -= __popc(wb[j]);
+          if (w >= w0 && w < w1 && wb[j]) {
+            lo_pos = min(lo_pos, p2);
+            hi_pos = max(hi_pos, p2 + __popc(wb[j]) - 1);
+          }
+        }
+        if (hi_pos >= 0) {
+          atomicMin(&s_range[0], lo_pos);
+          atomicMax(&s_range[1], hi_pos);
+        }
+      }
+      __syncthreads();
+      if (p.pad > 1 && total > 0 && s_range[1] == total - 1) {
         const int padded = (total + p.pad - 1) / p.pad * p.pad;
         const int32_t last = p.union_out[total - 1];
         for (int i = total + tid; i < padded; i += kTopkThreads) p.union_out[i] = last;
@@ -1022,7 +1033,7 @@ extern "C" int ps_select_union(const float* logits, const float* bias, int rows,
   uint8_t* base = static_cast<uint8_t*>(ws);
   // one CTA per row and per SM (the kernel's shared memory): all resident
   // at once iff rows <= SMs, and every CTA owns <= 512 words
-  prm.coresident = rows <= ps_num_sms() && rows <= kTopkThreads && (cols + 31) / 32 <= (size_t)rows * kTopkThreads;
+  prm.coresident = rows <= ps_num_sms() && (cols + 31) / 32 <= (size_t)kUnionWPT * kTopkThreads;
   prm.tickets = reinterpret_cast<int*>(base);
   prm.group_bits = reinterpret_cast<uint32_t*>(base + head);
   prm.row_bits = prm.group_bits + su_groups(rows) * su_words(cols);
