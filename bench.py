@@ -87,6 +87,7 @@ class ClockSampler:
         self.index = index
         self.samples = []
         self._stop = threading.Event()
+        self._ready = threading.Event()  # set once the sampler is live (NVML init can take ~100 ms)
         self._t = None
 
     def _run(self):
@@ -97,6 +98,8 @@ class ClockSampler:
             hd = nv.nvmlDeviceGetHandleByIndex(self.index)
             bits = [nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
                     nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap]
+            nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM)
+            self._ready.set()
             while not self._stop.is_set():
                 sm = nv.nvmlDeviceGetClockInfo(hd, nv.NVML_CLOCK_SM)
                 mx = nv.nvmlDeviceGetMaxClockInfo(hd, nv.NVML_CLOCK_SM)
@@ -106,6 +109,7 @@ class ClockSampler:
             return
         except Exception:
             pass
+        self._ready.set()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -120,6 +124,8 @@ class ClockSampler:
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(timeout=10)
+        self.samples.clear()  # only samples taken inside the timed region count
         return self
 
     def __exit__(self, *a):
