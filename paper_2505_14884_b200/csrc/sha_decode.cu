@@ -107,14 +107,16 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int n_units = p.B * p.top_k;
-  const int bid = blockIdx.x;
+  // the B zero-fill CTAs come first (they overlap the main work instead of
+  // forming a tail); stream-K CTA index = blockIdx.x - B
+  const int bid = (int)blockIdx.x - p.B;
   griddep_wait();  // q / KV / sel / lengths come from the preceding launches
   // (griddep_launch only after the main loop: with several waves of CTAs, an
   // early trigger lets the next grid's CTAs park on SM slots this grid needs)
 
-  if (bid >= p.n_ctas) {
+  if (bid < 0) {
     // ---- zero-fill CTA for sequence b: heads of non-selected groups = 0.0
-    const int b = bid - p.n_ctas;
+    const int b = (int)blockIdx.x;
     int* sel_flag = reinterpret_cast<int*>(smem);
     for (int g = tid; g < p.H_kv; g += kThreads) sel_flag[g] = 0;
     __syncthreads();
@@ -461,12 +463,14 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int n_units = p.B * p.top_k;
-  const int bid = blockIdx.x;
+  // the B zero-fill CTAs come first (they overlap the main work instead of
+  // forming a tail); stream-K CTA index = blockIdx.x - B
+  const int bid = (int)blockIdx.x - p.B;
   griddep_wait();
 
-  if (bid >= p.n_ctas) {
+  if (bid < 0) {
     // ---- zero-fill CTA for sequence b: heads of non-selected groups = 0.0
-    const int b = bid - p.n_ctas;
+    const int b = (int)blockIdx.x;
     int* sel_flag = reinterpret_cast<int*>(smem);
     for (int g = tid; g < p.H_kv; g += kThreads) sel_flag[g] = 0;
     __syncthreads();
