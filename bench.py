@@ -60,6 +60,11 @@ def parse():
     ap.add_argument("--union", type=float, default=0.5, help="target |S|/D of the MLP union")
     ap.add_argument("--kv-ring", type=int, default=0, help="alias KV storage over this many buffers (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--tp", action="store_true",
+                    help="tensor parallel over the torchrun ranks (heads + neurons sharded, routers replicated, "
+                         "NCCL all-reduce after the O- and down-projections); default: data-parallel replicas")
+    ap.add_argument("--distinct-layers", type=int, default=0,
+                    help="TP: distinct weight sets cycled over the layers (0 = all distinct)")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
     ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
     ap.add_argument("--concurrent-head-router", action="store_true",
@@ -292,16 +297,28 @@ def run_ours(args):
     B, ctx = args.batch, args.ctx
     L, H, H_kv, d_h, D = cfg.layers, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.ffn_dim
     cap = ctx + args.warmup * 2 + args.steps * 3 + 8
-    kv_layer = B * H_kv * cap * d_h * 2 * 2
     free = torch.cuda.mem_get_info(dev)[0]
-    model = DeviceModel.random(cfg, seed=1234 + rank, device=dev)
+    tp = None
+    if args.tp:
+        # every rank holds KV groups [r*H_kv/T, ...) + their heads and neurons
+        # [r*D/T, ...); routers are replicated (identical seeds on all ranks)
+        from paper_2505_14884_b200.parallel import TPPlan, TensorParallel, random_shard
+
+        plan = TPPlan.make(cfg, world, rank)
+        tp = TensorParallel(plan)
+        model = random_shard(cfg, plan, seed=1234, device=dev, distinct_layers=args.distinct_layers or None)
+        H_loc, Hkv_loc, D_loc = plan.heads_local, plan.kv_heads_local, plan.ffn_local
+    else:
+        model = DeviceModel.random(cfg, seed=1234 + rank, device=dev)
+        H_loc, Hkv_loc, D_loc = H, H_kv, D
+    kv_layer = B * Hkv_loc * cap * d_h * 2 * 2
     budget = free - model.weight_bytes() - 12 * 2 ** 30
     ring = args.kv_ring or (L if kv_layer * L <= budget else max(2, int(budget // kv_layer)))
     ring = min(ring, L)
 
     k_h = math.ceil(args.rho * H_kv - 1e-9)
     k_mlp = max(1, int(round(args.union * D)))
-    gen = np.random.default_rng(7 + rank)
+    gen = np.random.default_rng(7 + (0 if tp is not None else rank))
     sparse_relu = cfg.activation == "relu"
     hr = [pb.HeadRouter(cfg.model_dim, H_kv, seed=100 + ell, device=dev) for ell in range(L)]
     mr = None
@@ -311,15 +328,23 @@ def run_ours(args):
     polar = SparsityPolicy(mode="polar", head_density=args.rho,
                            mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
     eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring,
-                       router_backend=args.router_backend, concurrent_router=args.concurrent_head_router)
+                       router_backend=args.router_backend, concurrent_router=args.concurrent_head_router, tp=tp)
     eng.fill_random(ctx, seed=99 + rank)
-    dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches)
+    dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches, tp=tp)
     tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()
     out_host = torch.empty(B, dtype=torch.int64).pin_memory()
     eng.tokens.copy_(tokens_host)
     dense.tokens.copy_(tokens_host)
-    eng.capture()
-    dense.capture()
+    graphs = True
+    try:
+        eng.capture()
+        dense.capture()
+    except Exception as exc:  # e.g. a collective that cannot be captured: time eager steps
+        if tp is None:
+            raise
+        graphs = False
+        eng.graph = dense.graph = None
+        print(f"[bench] TP step not graph-capturable ({type(exc).__name__}); timing eager steps", file=sys.stderr)
 
     def barrier():
         if world > 1:
@@ -343,7 +368,10 @@ def run_ours(args):
 
     def replay(engine):
         def f():
-            engine.graph.replay()
+            if engine.graph is not None:
+                engine.graph.replay()
+            else:
+                engine.step_launches()
             engine._advance()
         return f
 
@@ -365,7 +393,10 @@ def run_ours(args):
     # e2e: host tokens in, host next-tokens out, through the engine API
     def e2e_step():
         eng.tokens.copy_(tokens_host, non_blocking=True)
-        eng.graph.replay()
+        if eng.graph is not None:
+            eng.graph.replay()
+        else:
+            eng.step_launches()
         eng._advance()
         out_host.copy_(eng.next_tokens, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -379,23 +410,25 @@ def run_ours(args):
 
     # roofline: the SHA kernel alone on the same caches, one launch per layer
     qkv = eng.qkv
-    sel = torch.stack([torch.randperm(H_kv, device=dev)[:k_h].sort().values for _ in range(B)]).to(torch.int32)
-    out = torch.empty(B, cfg.model_dim, dtype=torch.bfloat16, device=dev)
+    k_loc = max(1, min(k_h, Hkv_loc))
+    sel = torch.stack([torch.randperm(Hkv_loc, device=dev)[:k_loc].sort().values for _ in range(B)]).to(torch.int32)
+    dq = H_loc * d_h
+    out = torch.empty(B, dq, dtype=torch.bfloat16, device=dev)
     lens = [c.host_lengths.copy() for c in eng.caches]
     for c in eng.caches[:2]:
-        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H, eng.scale, out, cfg.model_dim,
+        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H_loc, eng.scale, out, dq,
                            max_len_hint=int(c.host_lengths.max()))
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s_ev.record(st)
     for c in eng.caches:
-        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H, eng.scale, out, cfg.model_dim,
+        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H_loc, eng.scale, out, dq,
                            max_len_hint=int(c.host_lengths.max()))
     e_ev.record(st)
     torch.cuda.synchronize()
     sha_ms = s_ev.elapsed_time(e_ev) / L
-    sha_bytes = float(np.mean([sha_algorithmic_bytes(l, k_h, H // H_kv, d_h, B, H) for l in lens]))
+    sha_bytes = float(np.mean([sha_algorithmic_bytes(l, k_loc, H // H_kv, d_h, B, H_loc) for l in lens]))
     hbm_peak, _, peak_kind = load_peaks()
     achieved = sha_bytes / (sha_ms * 1e-3) / 1e9
     traffic = ncu_traffic("sha_mma_kernel", args)
@@ -406,7 +439,8 @@ def run_ours(args):
     if sparse_relu:
         x2 = torch.randn(B, cfg.model_dim, device=dev).to(torch.bfloat16)
         y = torch.empty(B, cfg.model_dim, dtype=torch.float32, device=dev)
-        hot_idx = torch.from_numpy(np.sort(gen.choice(D, k_mlp, replace=False))).to(dev, torch.int32)
+        k_loc_mlp = min(k_mlp, D_loc)
+        hot_idx = torch.from_numpy(np.sort(gen.choice(D_loc, k_loc_mlp, replace=False))).to(dev, torch.int32)
         nit = pb.NeuronIndexTensor(0, hot_idx, validate=False)
         hidden = eng.hidden
         pk.mlp_into(model.layers[0].mlp, x2, nit.buffer, nit.count, hidden, y)
@@ -417,11 +451,12 @@ def run_ours(args):
         e_ev.record(st)
         torch.cuda.synchronize()
         mlp_ms = s_ev.elapsed_time(e_ev) / L
-        mlp_bytes = 2 * k_mlp * cfg.model_dim * 2 + k_mlp * 4 + cfg.model_dim * 4 + 2 * B * cfg.model_dim * 2 + k_mlp * 4
+        mlp_bytes = (2 * k_loc_mlp * cfg.model_dim * 2 + k_loc_mlp * 4 + cfg.model_dim * 4 + 2 * B * cfg.model_dim * 2
+                     + k_loc_mlp * 4)
 
     line = None
     if rank == 0:
-        toks = world * B * args.steps
+        toks = (1 if tp is not None else world) * B * args.steps  # TP ranks share one global batch
         value = toks / (ms_polar * 1e-3)
         dense_value = toks / (ms_dense * 1e-3)
         cpu = None
@@ -434,9 +469,11 @@ def run_ours(args):
         line = {
             "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_polar / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong" if tp is not None else "weak", "vs_baseline": None,
+            "dtype": "bf16",
             "data": "synthetic (random-init weights N(0,0.02); N(0,1) KV history; hot-neuron router bias)",
-            "config": dict(workload_config(args, cfg), kv_storage_buffers=ring,
+            "config": dict(workload_config(args, cfg), kv_storage_buffers=ring, graph_captured=graphs,
+                           parallelism=f"tp{world}" if tp is not None else f"dp{world}",
                            kv_aliasing=("none" if ring == L else f"K/V storage aliased over {ring} buffers")),
             "dense": {"value": dense_value, "ms_per_step": ms_dense / args.steps},
             "speedup_vs_dense": value / dense_value,
