@@ -3,6 +3,8 @@
 // top-k.  Ordering contract (tensors.py:54-73, numpy stable argsort of
 // -scores): value descending, ties -> lower index, -0.0 == +0.0, NaN ranks
 // below -inf (NaNs tied among themselves by index); ids written ascending.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ps {
@@ -976,7 +978,12 @@ int launch_head_router(const uint16_t* x, int64_t x_ld, const uint16_t* w_t, con
       return PS_ERR_CUDA;
     configured = true;
   }
-  const int csize = H < 8 ? H : 8;
+  static const int cmax = [] {
+    const char* e = getenv("PS_HR_CLUSTER");  // tuning hook: CTAs per row group (1..8)
+    const int v = e ? atoi(e) : 4;  // 4 measured best on B200 (B=64, H_kv=32)
+    return v < 2 ? 2 : (v > 8 ? 8 : v);
+  }();
+  const int csize = H < cmax ? H : cmax;
   const int HB = (H + csize - 1) / csize;
   const int groups = (B + R - 1) / R;
   return launch_ex(kern, dim3(groups * csize), dim3(kHrThreads), smem, st, csize, x, x_ld, w_t, bias, B, d, H, HB, k,
