@@ -49,7 +49,7 @@ PS_DEV int block_excl_scan(int v, int* s_warp, int* total) {
 
 constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
-constexpr int kTopkSmemCols = 40960;  // rows up to this width are staged in shared memory (160 KB)
+constexpr int kTopkSmemCols = 36864;  // rows up to this width are staged in shared memory (144 KB; 220 KB total)
 constexpr int kSample = 2048;         // strided sample of a row that brackets the k-th key
 constexpr int kMaxCand = 3072;        // keys inside the bracket kept for the exact select
 constexpr int kGroupRows = 16;        // union: rows ORed by the last CTA of each row group
@@ -68,7 +68,7 @@ struct TopkParams {
   // fused union (ps_select_union): per-row words, per-group words, tickets
   uint32_t* row_bits;    // (rows, words) or NULL
   uint32_t* group_bits;  // (groups, words)
-  int* tickets;          // [groups] + [1] + barrier {count, gen} + [rows] totals (self-resetting)
+  int* tickets;          // [groups] + [1] + 8-byte barrier word + spare (self-resetting)
   int coresident;        // every row CTA is resident at once: grid barrier + distributed union
   int lo, hi, pad;
   int32_t* union_out;
@@ -109,31 +109,58 @@ PS_DEV void select_bin(const int* g, int bins, int remaining, int* s_warp, int* 
   __syncthreads();
 }
 
-// select_bin for two ranks in one scan: s_sel = {bin1, rem1, cnt1, bin2, rem2, cnt2}
-template <int NT>
-PS_DEV void select_bin2(const int* g, int bins, int r1, int r2, int* s_warp, int* s_sel) {
-  const int per = bins / NT;
-  const int hi = bins - (int)threadIdx.x * per;
-  int loc = 0;
-  for (int j = 1; j <= per; ++j) loc += g[hi - j];
-  const int above = block_excl_scan<NT>(loc, s_warp, nullptr);
+// Block form of select_bin for up to two (histogram, rank) pairs at once
+// (r2 <= 0: none), with two block barriers: warp w owns bins
+// [BINS - (w+1)*BINS/16, BINS - w*BINS/16) (warp 0 the highest), each lane
+// PER contiguous bins; warp scans, then a 16-entry scan of the warp totals
+// through shared memory.  out = {bin, remaining within the bin, bin count}.
+template <int BINS, int NT>
+PS_DEV void bsel2(const int* g1, int r1, int* o1, const int* g2, int r2, int* o2, int* s_wt) {
+  constexpr int NW = NT / 32, PER_W = BINS / NW, PER = PER_W / 32;
+  static_assert(PER >= 1 && NW <= 32, "bsel2 shape");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lo = BINS - warp * PER_W - (lane + 1) * PER;
+  int a1 = 0, a2 = 0;
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int r = t ? r2 : r1;
-    if (above < r && above + loc >= r) {
+  for (int j = 0; j < PER; ++j) {
+    a1 += g1[lo + j];
+    if (r2 > 0) a2 += g2[lo + j];
+  }
+  int x1 = a1, x2 = a2;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y1 = __shfl_up_sync(0xffffffffu, x1, o), y2 = __shfl_up_sync(0xffffffffu, x2, o);
+    if (lane >= o) { x1 += y1; x2 += y2; }
+  }
+  if (lane == 31) { s_wt[warp] = x1; s_wt[32 + warp] = x2; }
+  __syncthreads();
+  int w1 = lane < NW ? s_wt[lane] : 0, w2 = lane < NW ? s_wt[32 + lane] : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y1 = __shfl_up_sync(0xffffffffu, w1, o), y2 = __shfl_up_sync(0xffffffffu, w2, o);
+    if (lane >= o) { w1 += y1; w2 += y2; }
+  }
+  // exclusive prefix of this warp = inclusive of warp-1
+  const int b1 = __shfl_sync(0xffffffffu, w1, (warp + 31) & 31), b2 = __shfl_sync(0xffffffffu, w2, (warp + 31) & 31);
+  auto find = [&](const int* g, int r, int base, int x, int a, int* o) {
+    const int above = (warp ? base : 0) + x - a;
+    if (r > 0 && above < r && above + a >= r) {
       int cum = above;
-      for (int j = 1; j <= per; ++j) {
-        const int c = g[hi - j];
+#pragma unroll
+      for (int b = lo + PER - 1; b >= lo; --b) {
+        const int c = g[b];
         if (cum + c >= r) {
-          s_sel[3 * t] = hi - j;
-          s_sel[3 * t + 1] = r - cum;
-          s_sel[3 * t + 2] = c;
+          o[0] = b;
+          o[1] = r - cum;
+          o[2] = c;
           break;
         }
         cum += c;
       }
     }
-  }
+  };
+  find(g1, r1, b1, x1, a1, o1);
+  find(g2, r2, b2, x2, a2, o2);
   __syncthreads();
 }
 
@@ -141,32 +168,38 @@ PS_DEV void select_bin2(const int* g, int bins, int r1, int r2, int* s_warp, int
 // (12/10/10 bits).  Returns the key; *eq = how many keys equal it, *rem =
 // how many of those reach rank r.  Block-wide; r in [1, n].
 template <int NT>
-PS_DEV uint32_t list_select(const uint32_t* keys, int n, int r, int* hist, int* s_warp, int* s_sel, int* eq,
+PS_DEV uint32_t list_select(const uint32_t* keys, int n, int r, int* hA, int* hB, int* s_sel, int* s_wt, int* eq,
                             int* rem) {
+  // hA [4096] serves passes 0 and 2, hB [1024] pass 1; hA is re-zeroed
+  // during pass 1, so each pass costs two block barriers
   const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 4096; i += NT) hA[i] = 0;
+  for (int i = threadIdx.x; i < 1024; i += NT) hB[i] = 0;
+  __syncthreads();
   uint32_t prefix = 0, mask = 0;
   int remaining = r;
 #pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = pass == 0 ? 20 : (pass == 1 ? 10 : 0);
     const int bins = pass == 0 ? 4096 : 1024;
-    for (int i = threadIdx.x; i < bins; i += NT) hist[i] = 0;
-    __syncthreads();
+    int* h = pass == 1 ? hB : hA;
     for (int base = 0; base < n; base += NT) {
       const int i = base + (int)threadIdx.x;
       const uint32_t u = i < n ? keys[i] : 0u;
-      hist_add_agg(hist, i < n && (u & mask) == prefix, (u >> shift) & (uint32_t)(bins - 1), lane);
+      hist_add_agg(h, i < n && (u & mask) == prefix, (u >> shift) & (uint32_t)(bins - 1), lane);
     }
+    if (pass == 1)
+      for (int i = threadIdx.x; i < 1024; i += NT) hA[i] = 0;
     __syncthreads();
-    select_bin<NT>(hist, bins, remaining, s_warp, s_sel);
+    if (pass == 0) bsel2<4096, NT>(h, remaining, s_sel, h, 0, s_sel, s_wt);
+    else bsel2<1024, NT>(h, remaining, s_sel, h, 0, s_sel, s_wt);
     prefix |= (uint32_t)s_sel[0] << shift;
     remaining = s_sel[1];
     mask |= (uint32_t)(bins - 1) << shift;
   }
   *eq = s_sel[2];
   *rem = remaining;
-  __syncthreads();  // s_sel is reused by the caller
-  return prefix;
+  return prefix;  // s_sel is next written only after another block barrier
 }
 
 // debug: per-CTA globaltimer stamps of the phases (ps_debug_topk_trace)
@@ -263,11 +296,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   int* hist = reinterpret_cast<int*>(smem);                          // [4096]
   uint32_t* samp = reinterpret_cast<uint32_t*>(hist + 4096);         // [kMaxCand] samples, then tied cols
   uint32_t* wc_key = samp + kMaxCand;                                // [kMaxCand] per-warp lists
+  // [2048] second-level histograms: used by the bracket before the per-warp
+  // lists are filled and by list_select after they were compacted
+  int* hist2 = reinterpret_cast<int*>(wc_key);
   int* wc_idx = reinterpret_cast<int*>(wc_key + kMaxCand);           // [kMaxCand]
   uint32_t* cand_key = reinterpret_cast<uint32_t*>(wc_idx + kMaxCand);  // [kMaxCand] compacted
   int* cand_idx = reinterpret_cast<int*>(cand_key + kMaxCand);       // [kMaxCand]
   uint32_t* keys = reinterpret_cast<uint32_t*>(cand_idx + kMaxCand);  // [cols] if staged
-  __shared__ int s_warp[32];
+  __shared__ int s_warp[64];
   __shared__ int s_eq[kTopkWarps], s_gt[kTopkWarps], s_wn[kTopkWarps];
   __shared__ int s_sel[6];
   __shared__ int s_na, s_ovf, s_n2, s_last;
@@ -279,6 +315,20 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   const bool staged = !threshold && cols <= kTopkSmemCols;
   auto logit = [&](int i) -> float { return bias ? __ldg(x + i) + __ldg(bias + i) : __ldg(x + i); };
   auto key_at = [&](int i) -> uint32_t { return staged ? keys[i] : order_key(logit(i)); };
+  const bool vec_ok = staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0 &&
+                      (!bias || ((uintptr_t)bias & 15) == 0);
+  const bool fused = vec_ok && cols <= kRegCols;
+  if (fused && bias) {
+    // the bias is static: copy it into the key slots before waiting on the
+    // previous kernel; each thread later reads back only its own slots
+    const float4* b4 = reinterpret_cast<const float4*>(bias);
+#pragma unroll
+    for (int j = 0; j < kRegVec; ++j) {
+      const int i = j * kTopkThreads + tid;
+      if (i < (cols >> 2)) cp_async16(keys + 4 * i, b4 + i, 16);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   griddep_wait();
   griddep_launch();
   TK_STAMP(0);
@@ -289,10 +339,9 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   if (!threshold) {
     if (tid == 0) { s_na = 0; s_ovf = 0; s_n2 = 0; }
     for (int i = tid; i < 4096; i += kTopkThreads) hist[i] = 0;
+    for (int i = tid; i < 2048; i += kTopkThreads) hist2[i] = 0;
     const int S = min(cols, kSample);
     const int stride = cols / S;
-    const bool vec_ok = staged && (cols & 3) == 0 && (p.ld & 3) == 0 && ((uintptr_t)x & 15) == 0 &&
-                        (!bias || ((uintptr_t)bias & 15) == 0);
     const float q = (float)p.k / (float)cols;
     const float rs = q * (float)S;
     const float dl = 3.f * sqrtf(fmaxf(rs * (1.f - q), 0.f)) + 2.f;
@@ -301,29 +350,31 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
     const int r_lo = max(1, min(S, (int)ceilf(rs + dl)));
     // bracket (22-bit sample order statistics at ranks r_hi / r_lo) from samp[0, S)
     auto bracket = [&](uint32_t& hi22, uint32_t& lo22) {
+      // hist (top 12 bits) and hist2 (next 10 bits, one half per rank) were
+      // zeroed at entry; warp 0 scans, 4 block barriers in all
       for (int base = 0; base < S; base += kTopkThreads) {
         const int j = base + tid;
         const uint32_t u = j < S ? samp[j] : 0u;
         hist_add_agg(hist, j < S, u >> 20, lane);
       }
       __syncthreads();
-      select_bin2<kTopkThreads>(hist, 4096, r_hi, r_lo, s_warp, s_sel);
+      TK_STAMP(12);
+      bsel2<4096, kTopkThreads>(hist, r_hi, s_sel, hist, r_lo, s_sel + 3, s_warp);
+      TK_STAMP(13);
       const int bin_hi = s_sel[0], rem_hi = s_sel[1], bin_lo = s_sel[3], rem_lo = s_sel[4];
-      for (int i = tid; i < 2048; i += kTopkThreads) hist[i] = 0;
-      __syncthreads();
       for (int base = 0; base < S; base += kTopkThreads) {
         const int j = base + tid;
         const uint32_t u = j < S ? samp[j] : 0u;
         const int top = (int)(u >> 20);
         const uint32_t sub = (u >> 10) & 1023u;
-        hist_add_agg(hist, j < S && top == bin_hi, sub, lane);
-        hist_add_agg(hist + 1024, j < S && top == bin_lo, sub, lane);
+        hist_add_agg(hist2, j < S && top == bin_hi, sub, lane);
+        hist_add_agg(hist2 + 1024, j < S && top == bin_lo, sub, lane);
       }
       __syncthreads();
-      select_bin<kTopkThreads>(hist, 1024, rem_hi, s_warp, s_sel);
+      TK_STAMP(14);
+      bsel2<1024, kTopkThreads>(hist2, rem_hi, s_sel, hist2 + 1024, rem_lo, s_sel + 3, s_warp);
       hi22 = open_top ? 0x3FFFFFu : (((uint32_t)bin_hi << 10) | (uint32_t)s_sel[0]);
-      select_bin<kTopkThreads>(hist + 1024, 1024, rem_lo, s_warp, s_sel);
-      lo22 = open_bottom ? 0u : (((uint32_t)bin_lo << 10) | (uint32_t)s_sel[0]);
+      lo22 = open_bottom ? 0u : (((uint32_t)bin_lo << 10) | (uint32_t)s_sel[3]);
     };
     int n_above_t = 0, wn = 0;  // this thread's count above the bracket; this warp's candidates
     uint32_t* wk = wc_key + warp * kWarpCand;
@@ -341,12 +392,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       wn += __popc(bal);
     };
     uint32_t hi22, lo22;
-    if (vec_ok && cols <= kRegCols) {
+    if (fused) {
       // ---- fused: the row's loads are in flight (registers) while the
       //      bracket is computed from a strided sample read directly from
       //      memory; then ONE pass converts, stages and classifies every key
       const float4* x4 = reinterpret_cast<const float4*>(x);
-      const float4* b4 = reinterpret_cast<const float4*>(bias);
       const int n4 = cols >> 2;
       float4 v[kRegVec];
 #pragma unroll
@@ -359,12 +409,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       TK_STAMP(1);
       bracket(hi22, lo22);
       TK_STAMP(2);
+      if (bias) asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
       for (int j = 0; j < kRegVec; ++j) {
         const int i = j * kTopkThreads + tid;
         const bool ok = i < n4;
         if (ok && bias) {
-          const float4 bb = __ldg(b4 + i);
+          const float4 bb = *reinterpret_cast<const float4*>(keys + 4 * i);
           v[j].x += bb.x; v[j].y += bb.y; v[j].z += bb.z; v[j].w += bb.w;
         }
         const uint4 u = ok ? make_uint4(order_key(v[j].x), order_key(v[j].y), order_key(v[j].z), order_key(v[j].w))
@@ -441,7 +492,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       TK_STAMP(3);
       // ---- 3. exact k-th key among the candidates, then the tie column
       int n_eq, rem;
-      prefix = list_select<kTopkThreads>(cand_key, n_cand, p.k - n_above, hist, s_warp, s_sel, &n_eq, &rem);
+      prefix = list_select<kTopkThreads>(cand_key, n_cand, p.k - n_above, hist, hist2, s_sel, s_warp, &n_eq, &rem);
       remaining = rem;
       if (rem < n_eq) {
         for (int base = 0; base < n_cand; base += kTopkThreads) {
@@ -458,7 +509,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
         }
         __syncthreads();
         int e2, r2;
-        const uint32_t v = list_select<kTopkThreads>(samp, s_n2, rem, hist, s_warp, s_sel, &e2, &r2);
+        const uint32_t v = list_select<kTopkThreads>(samp, s_n2, rem, hist, hist2, s_sel, s_warp, &e2, &r2);
         tie_lim = (int)~v + 1;  // the highest taken tied column + 1
       }
       if (p.trace && tid == 0) p.trace[blockIdx.x * 16 + 10] = ((unsigned long long)n_cand << 32) | (unsigned)n_eq;
@@ -498,8 +549,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       uint32_t bt = 0;
       const int e0 = w << 5;
       if (e0 + 32 <= cols) {
+        // the 8 quads are visited in a lane-rotated order: consecutive lanes'
+        // words are 128 bytes apart, so an unrotated walk is an 8-way conflict
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
+        for (int j = 0; j < 8; ++j) {
+          const int c4 = (j + lane) & 7;
           const uint4 u4 = *reinterpret_cast<const uint4*>(keys + e0 + 4 * c4);
           const uint32_t uu[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
@@ -594,24 +648,25 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
   if (p.row_bits) {
     const int groups = (p.rows + kGroupRows - 1) / kGroupRows;
     if (p.coresident) {
-      // every row CTA is resident (rows <= SMs, one CTA per SM): a grid
-      // barrier, then CTA c ORs words [w0, w1) over all rows, a second
-      // barrier publishes the per-CTA popcounts, and each CTA writes its
-      // ascending ids at its prefix -- no single-CTA tail
-      int* bar_count = p.tickets + groups + 1;
-      int* bar_gen = p.tickets + groups + 2;
-      int* totals = p.tickets + groups + 3;
+      // every row CTA is resident (rows <= SMs, one CTA per SM): one grid
+      // barrier, then each CTA writes the ascending ids of its own word
+      // range -- no single-CTA tail
+      // barrier word {gen:32 | count:32} (8-byte aligned inside the ticket
+      // head): the last arriver bumps gen and clears count in ONE atomic and
+      // does not wait; the others pass on count == rows or a changed gen
+      unsigned long long* bar = reinterpret_cast<unsigned long long*>(p.tickets + ((groups + 2) & ~1));
       auto grid_barrier = [&]() {
         __syncthreads();
         if (tid == 0) {
-          const int g = *reinterpret_cast<volatile int*>(bar_gen);
           __threadfence();
-          if (atomicAdd(bar_count, 1) == p.rows - 1) {
-            *bar_count = 0;
-            __threadfence();
-            atomicExch(bar_gen, g + 1);
+          const unsigned long long old = atomicAdd(bar, 1ull);
+          const uint32_t g = (uint32_t)(old >> 32);
+          if ((uint32_t)old == (uint32_t)p.rows - 1u) {
+            atomicAdd(bar, (1ull << 32) - (unsigned long long)p.rows);
           } else {
-            while (*reinterpret_cast<volatile int*>(bar_gen) == g) {
+            while (true) {
+              const unsigned long long v = *reinterpret_cast<volatile unsigned long long*>(bar);
+              if ((uint32_t)v == (uint32_t)p.rows || (uint32_t)(v >> 32) != g) break;
             }
           }
           __threadfence();
@@ -628,6 +683,35 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       const int w0 = wlo + (int)((long long)row * nw / p.rows), w1 = wlo + (int)((long long)(row + 1) * nw / p.rows);
       const int kw = (nw + kTopkThreads - 1) / kTopkThreads;  // contiguous words per thread (<= kUnionWPT)
       const int tw0 = wlo + tid * kw;
+      // OR over the rows with 16-byte loads; when the words are few the
+      // threads also split the rows (slices), ORed through shared memory
+      const int q0 = wlo >> 2, nq = ((whi + 3) >> 2) - q0;
+      const bool vec = (words & 3) == 0 && nq <= kTopkThreads;
+      const int slices = vec ? max(1, min(kTopkThreads / nq, 8)) : 0;
+      uint32_t* s_or = reinterpret_cast<uint32_t*>(hist);  // [slices][nq * 4]
+      if (vec) {
+        const int sl = tid / nq, qq = tid - sl * nq;
+        if (sl < slices) {
+          const uint4* rb = reinterpret_cast<const uint4*>(p.row_bits) + q0 + qq;
+          const int wq = words >> 2;
+          uint4 acc4 = make_uint4(0, 0, 0, 0);
+          for (int r0 = sl; r0 < p.rows; r0 += 8 * slices) {
+            uint4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int r = r0 + j * slices;
+              v[j] = r < p.rows ? __ldcg(rb + (size_t)r * wq) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              acc4.x |= v[j].x; acc4.y |= v[j].y; acc4.z |= v[j].z; acc4.w |= v[j].w;
+            }
+          }
+          reinterpret_cast<uint4*>(s_or)[sl * nq + qq] = acc4;
+        }
+        __syncthreads();
+      }
+      TK_STAMP(8);
       uint32_t wb[kUnionWPT];
       int cnt = 0;
 #pragma unroll
@@ -635,8 +719,18 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
         const int w = tw0 + j;
         uint32_t acc = 0;
         if (j < kw && w < whi) {
-#pragma unroll 8
-          for (int r = 0; r < p.rows; ++r) acc |= __ldcg(p.row_bits + (size_t)r * words + w);
+          if (vec) {
+            for (int sl = 0; sl < slices; ++sl) acc |= s_or[sl * nq * 4 + (w - 4 * q0)];
+          } else {
+            // 32 loads in flight per batch (one L2 round trip per 32 rows)
+            for (int r0 = 0; r0 < p.rows; r0 += 32) {
+              uint32_t v[32];
+#pragma unroll
+              for (int r = 0; r < 32; ++r) v[r] = r0 + r < p.rows ? __ldcg(p.row_bits + (size_t)(r0 + r) * words + w) : 0u;
+#pragma unroll
+              for (int r = 0; r < 32; ++r) acc |= v[r];
+            }
+          }
           const int top = p.hi - (w << 5);
           if (top < 32) acc &= (top <= 0) ? 0u : ((1u << top) - 1u);
         }
@@ -645,6 +739,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_rows_kernel(const TopkParam
       }
       int total;
       int pos = block_excl_scan<kTopkThreads>(cnt, s_warp, &total);
+      TK_STAMP(9);
 #pragma unroll
       for (int j = 0; j < kUnionWPT; ++j) {
         const int w = tw0 + j;

@@ -7,12 +7,15 @@ from paper_2505_14884_b200 import _lib  # noqa: E402
 
 dev = torch.device("cuda")
 L = _lib.load()
-names = ["start", "loaded", "bracket", "counted", "kth", "selected", "barrier1", "union", "-", "-"]
-for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"), (256, 16384, 8192, "hot")]:
+names = ["start", "loaded", "bracket", "counted", "kth", "selected", "barrier1", "union", "or-loaded", "scanned",
+         "-", "-", "br-hist1", "br-sel1", "br-hist2"]
+for rows, cols, k, dist, use_bias in [(64, 16384, 8192, "hot", False), (64, 16384, 8192, "hot", True),
+                                     (64, 1024, 512, "normal", False), (256, 16384, 8192, "hot", False)]:
     g = torch.Generator(device=dev); g.manual_seed(0)
     lg = torch.randn(rows, cols, device=dev, generator=g)
     if dist == "hot":
         lg[:, torch.randperm(cols, device=dev, generator=g)[: cols // 2]] += 20.0
+    bias = torch.randn(cols, device=dev, generator=g) if use_bias else None
     bm = torch.zeros((cols + 31) // 32, dtype=torch.int32, device=dev)
     nb = int(_lib.load().ps_select_union_workspace_bytes(rows, cols))
     ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
@@ -20,7 +23,7 @@ for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"),
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
     tk = torch.zeros(1, dtype=torch.int32, device=dev)
     tr = torch.zeros(rows * 8 * 16, dtype=torch.int64, device=dev)
-    f = lambda: _lib.call("ps_select_union", lg.data_ptr(), None, rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
+    f = lambda: _lib.call("ps_select_union", lg.data_ptr(), None if bias is None else bias.data_ptr(), rows, cols, cols, k, 0.0, ws.data_ptr(),  # noqa
                           nb, 0, cols, 128, buf.data_ptr(), cnt.data_ptr(), _lib.stream_ptr())
     for _ in range(3):
         f()
@@ -32,10 +35,10 @@ for rows, cols, k, dist in [(64, 16384, 8192, "hot"), (64, 1024, 512, "normal"),
     t = tr.view(-1, 16).cpu().numpy()
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
-    print(f"== {rows}x{cols} k={k} {dist}: CTAs={len(t)}  span={(max(t[:, 5].max(), t[:, 7].max()) - t0) / 1e3:.1f} us  "
+    print(f"== {rows}x{cols} k={k} {dist} bias={use_bias}: CTAs={len(t)}  span={(max(t[:, 5].max(), t[:, 7].max()) - t0) / 1e3:.1f} us  "
           f"fallbacks={int((t[:, 11] == 1).sum())}  cand(med)={int(np.median(t[:, 10] >> 32))} "
           f"eq(max)={int((t[:, 10] & 0xffffffff).max())}")
-    for j in range(1, 10):
+    for j in [1, 12, 13, 14, 2, 3, 4, 5, 6, 8, 9, 7]:
         v = t[:, j]
         ok = v > 0
         if ok.any():
