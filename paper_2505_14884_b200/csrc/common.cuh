@@ -197,6 +197,15 @@ PS_DEV void cp_async16(void* smem_dst, const void* gmem_src, uint32_t src_bytes)
                : "memory");
 }
 
+// same with an L2 prefetch-size hint: the 256-byte line pair holding the
+// source is fetched, so a row walked 128 bytes per pipeline stage finds its
+// next block in L2
+PS_DEV void cp_async16_l2_256(void* smem_dst, const void* gmem_src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src),
+               "r"(src_bytes)
+               : "memory");
+}
+
 // arrive on `bar` once all prior cp.async of this thread have landed
 // (noinc: the arrival counts toward the barrier's expected count).
 PS_DEV void cp_async_arrive_noinc(uint64_t* bar) {

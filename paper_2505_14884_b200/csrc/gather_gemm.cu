@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int r = 0; r < 8; ++r) {
               const int row = (lt >> 3) + 16 * r;
               const bool ok = kok && src[r] != nullptr;
-              cp_async16(sa + sw128(row, u), ok ? (const void*)(src[r] + k0) : (const void*)p.w, ok ? 16u : 0u);
+              cp_async16_l2_256(sa + sw128(row, u), ok ? (const void*)(src[r] + k0) : (const void*)p.w, ok ? 16u : 0u);
             }
           } else {
             // 64 K rows x 128 output features, MN-major SW128 atoms (8 K x 64 MN);
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 2)
               const void* srcp = ok ? (const void*)(p.w + (size_t)kid[r] * p.w_ld + gm) : (const void*)p.w;
               const uint32_t off = (uint32_t)((mu >> 3) * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 +
                                               (((mu & 7) ^ (kk & 7)) << 4));
-              cp_async16(sa + off, srcp, ok ? 16u : 0u);
+              cp_async16_l2_256(sa + off, srcp, ok ? 16u : 0u);
             }
 #pragma unroll
             for (int r = 0; r < 8; ++r) kid[r] = kid_next[r];

@@ -17,7 +17,7 @@ if OLD is not None:
     from paper_2505_14884_b200 import _lib  # noqa: E402
     for _n in ("ps_sha_workspace_bytes", "ps_sha_decode"):
         getattr(OLD, _n).restype, getattr(OLD, _n).argtypes = _lib.SIGNATURES[_n]
-for (B, H, H_kv, ctx, ks) in [(64, 32, 32, 1920, (16, 32)), (256, 32, 8, 1920, (4,))]:
+for (B, H, H_kv, ctx, ks) in [(64, 32, 32, 1920, (16,)), (256, 32, 8, 1920, (4, 8)), (64, 32, 8, 1920, (4, 8))]:
     n = 4
     caches = []
     for i in range(n):
