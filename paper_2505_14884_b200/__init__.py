@@ -9,6 +9,7 @@ compute call raises.
 """
 
 from .exceptions import CapacityError, ConfigurationError, EmptyCacheError, UndefinedRecallError
+from .fileio import LayerKTable, load_model, load_router, load_run_config, load_token_stream, save_token_stream
 from .kernels import (
     BatchHeadIndex,
     FlashBlockParams,
@@ -34,5 +35,6 @@ __all__ = [
     "dense_mlp_forward", "gqa_selective_attention_decode", "head_router_forward", "l2_norm_per_head",
     "mlp_router_forward", "selective_gemm", "selective_gemm_t", "selective_head_flash_attention_decode",
     "sparse_mlp_forward", "swiglu_mlp_forward", "topk_indices", "topk_indices_rows", "union_from_logits",
-    "union_neuron_indices",
+    "union_neuron_indices", "LayerKTable", "load_model", "load_router", "load_run_config", "load_token_stream",
+    "save_token_stream",
 ]

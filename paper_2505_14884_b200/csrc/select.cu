@@ -1078,7 +1078,9 @@ int launch_head_router(const uint16_t* x, int64_t x_ld, const uint16_t* w_t, con
     const int v = e ? atoi(e) : 4;  // 4 measured best on B200 (B=64, H_kv=32)
     return v < 2 ? 2 : (v > 8 ? 8 : v);
   }();
-  const int csize = H < cmax ? H : cmax;
+  // >= 2: the kernel uses cluster barriers / DSMEM, which need a cluster
+  // launch (a CTA of the pair may own no head, e.g. H == 1)
+  const int csize = H < 2 ? 2 : (H < cmax ? H : cmax);
   const int HB = (H + csize - 1) / csize;
   const int groups = (B + R - 1) / R;
   return launch_ex(kern, dim3(groups * csize), dim3(kHrThreads), smem, st, csize, x, x_ld, w_t, bias, B, d, H, HB, k,

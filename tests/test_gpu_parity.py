@@ -408,7 +408,8 @@ def test_routers_match_reference(golden):
 
 def test_head_router_topk_bit_exact_given_logits():
     rng = np.random.default_rng(9)
-    for B, d, H, k in [(64, 4096, 32, 16), (512, 4096, 8, 4), (256, 9216, 72, 22), (3, 256, 8, 4)]:
+    for B, d, H, k in [(64, 4096, 32, 16), (512, 4096, 8, 4), (256, 9216, 72, 22), (3, 256, 8, 4),
+                       (5, 256, 1, 1), (7, 128, 3, 2), (2, 512, 72, 72)]:  # MQA, odd H, k == H
         hr = pb.HeadRouter(d, H, seed=B)
         x = t(po.round_bf16(rng.normal(size=(B, d)).astype(np.float32)))
         logits = torch.empty((B, H), dtype=torch.float32, device=DEV)
