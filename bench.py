@@ -67,6 +67,8 @@ def parse():
                     help="TP: distinct weight sets cycled over the layers (0 = all distinct)")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
     ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
+    ap.add_argument("--kv-page-rows", type=int, default=0,
+                    help="paged KV caches with this many rows per page (0 = contiguous)")
     ap.add_argument("--concurrent-head-router", action="store_true",
                     help="head router as a concurrent graph branch instead of fused with the KV append")
     return ap.parse_args()
@@ -266,6 +268,7 @@ def workload_config(args, cfg):
             "seq_len": args.ctx, "head_density": args.rho, "union_density": args.union,
             "layers": cfg.layers, "d_model": cfg.model_dim, "ffn": cfg.ffn_dim, "heads": cfg.heads,
             "kv_heads": cfg.kv_heads, "parallelism": f"dp{args.gpus}",
+            "kv_layout": f"paged ({args.kv_page_rows} rows/page)" if args.kv_page_rows else "contiguous",
             "l2": "inputs larger than L2 (KV cache >> 126 MB); no flush"}
 
 
@@ -328,7 +331,8 @@ def run_ours(args):
     polar = SparsityPolicy(mode="polar", head_density=args.rho,
                            mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
     eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring,
-                       router_backend=args.router_backend, concurrent_router=args.concurrent_head_router, tp=tp)
+                       router_backend=args.router_backend, concurrent_router=args.concurrent_head_router, tp=tp,
+                       kv_page_rows=args.kv_page_rows)
     eng.fill_random(ctx, seed=99 + rank)
     dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches, tp=tp)
     tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()

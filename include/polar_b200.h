@@ -95,6 +95,29 @@ int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths,
                  const void* k_new, const void* v_new, int64_t src_ld,
                  int B, int H_kv, int cap, int d_h, int32_t* err_flag, void* stream);
 
+/* Paged KV cache (the reference cache is contiguous,
+ * tensors.py:116-213).  K and V live in pools of `pool_pages` pages of
+ * layout (page, H_kv, page_rows, d_h) bf16; logical row r of sequence b is
+ * row r % page_rows of page block_table[b * table_ld + r / page_rows], so
+ * the logical capacity is table_ld * page_rows.  page_rows must be a
+ * multiple of the SHA tile (4096 / d_h rows; 32 at d_h = 128).  Every one
+ * of a row's table_ld entries must be readable (entries past a sequence's
+ * length are prefetched as hints and never dereferenced).
+ * ps_sha_decode_paged: ps_sha_decode over the paged pools (same math, same
+ *   workspace query, same error behaviour).
+ * ps_kv_append_paged: ps_kv_append into the page holding lengths[b]
+ *   (the caller maps that page before the step). */
+int ps_sha_decode_paged(const void* q, int64_t q_ld, const void* k_pool, const void* v_pool,
+                        int pool_pages, int page_rows, const int32_t* block_table, int64_t table_ld,
+                        const int32_t* lengths, const int32_t* sel, int group_base,
+                        int B, int H, int H_kv, int d_h, int top_k,
+                        float scale, int num_splits, int max_len_hint,
+                        void* out, int64_t out_ld, int out_dtype,
+                        void* ws, size_t ws_bytes, void* stream);
+int ps_kv_append_paged(void* k_pool, void* v_pool, int page_rows, const int32_t* block_table,
+                       int64_t table_ld, int32_t* lengths, const void* k_new, const void* v_new,
+                       int64_t src_ld, int B, int H_kv, int d_h, int32_t* err_flag, void* stream);
+
 /* ======================================================================
  * Selection (bit-exact with the reference ordering: value descending,
  * ties -> lower index, -0.0 == +0.0, NaN below -inf).

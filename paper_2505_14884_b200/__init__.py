@@ -25,13 +25,13 @@ from .kernels import (
     union_neuron_indices,
 )
 from .routers import HeadRouter, MlpRouter, head_router_forward, mlp_router_forward, union_from_logits
-from .tensors import KVCache, l2_norm_per_head, topk_indices, topk_indices_rows
+from .tensors import KVCache, PagedKVCache, l2_norm_per_head, topk_indices, topk_indices_rows
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchHeadIndex", "CapacityError", "ConfigurationError", "EmptyCacheError", "FlashBlockParams",
-    "HeadRouter", "KVCache", "MlpRouter", "NeuronIndexTensor", "PackedMLP", "UndefinedRecallError",
+    "HeadRouter", "KVCache", "PagedKVCache", "MlpRouter", "NeuronIndexTensor", "PackedMLP", "UndefinedRecallError",
     "dense_mlp_forward", "gqa_selective_attention_decode", "head_router_forward", "l2_norm_per_head",
     "mlp_router_forward", "selective_gemm", "selective_gemm_t", "selective_head_flash_attention_decode",
     "sparse_mlp_forward", "swiglu_mlp_forward", "topk_indices", "topk_indices_rows", "union_from_logits",

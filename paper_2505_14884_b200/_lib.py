@@ -38,6 +38,9 @@ SIGNATURES = {
     "ps_sha_decode": (_i, [_vp, _i64, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _i,
                            _vp, _i64, _i, _vp, _sz, _vp]),
     "ps_kv_append": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _i, _i, _i, _i, _vp, _vp]),
+    "ps_sha_decode_paged": (_i, [_vp, _i64, _vp, _vp, _i, _i, _vp, _i64, _vp, _vp, _i, _i, _i, _i, _i, _i, _f, _i,
+                                 _i, _vp, _i64, _i, _vp, _sz, _vp]),
+    "ps_kv_append_paged": (_i, [_vp, _vp, _i, _vp, _i64, _vp, _vp, _vp, _i64, _i, _i, _i, _vp, _vp]),
     "ps_topk_rows": (_i, [_vp, _i, _i, _i64, _i, _vp, _vp, _vp]),
     "ps_threshold_rows": (_i, [_vp, _i, _i, _i64, _f, _vp, _vp]),
     "ps_select_union_workspace_bytes": (_sz, [_i, _i]),

@@ -18,7 +18,9 @@ __global__ void __launch_bounds__(kKvThreads) kv_append_kernel(uint16_t* __restr
                                                                int32_t* __restrict__ lengths,
                                                                const uint16_t* __restrict__ kn,
                                                                const uint16_t* __restrict__ vn, int64_t src_ld,
-                                                               int H_kv, int cap, int d_h, int32_t* err_flag) {
+                                                               int H_kv, int cap, int d_h, int32_t* err_flag,
+                                                               const int32_t* __restrict__ table, int64_t table_ld,
+                                                               int page_rows) {
   const int b = blockIdx.x;
   griddep_wait();
   griddep_launch();
@@ -26,6 +28,17 @@ __global__ void __launch_bounds__(kKvThreads) kv_append_kernel(uint16_t* __restr
   if (pos >= cap) {
     if (threadIdx.x == 0 && err_flag) *err_flag = 1;
     return;
+  }
+  // row base of (b, head 0) at `pos`; heads are `hstride` rows apart
+  size_t base;
+  size_t hstride;
+  if (table) {  // paged pool (pages, H_kv, page_rows, d_h)
+    const int pg = __ldg(table + (size_t)b * table_ld + pos / page_rows);
+    base = (size_t)pg * H_kv * page_rows + pos % page_rows;
+    hstride = page_rows;
+  } else {
+    base = (size_t)b * H_kv * cap + pos;
+    hstride = cap;
   }
   const int vec_per_head = d_h / 8;
   const int total = H_kv * vec_per_head;
@@ -46,7 +59,7 @@ __global__ void __launch_bounds__(kKvThreads) kv_append_kernel(uint16_t* __restr
       const int e = e0 + j * kKvThreads + threadIdx.x;
       if (e < total) {
         const int h = e / vec_per_head, c = e - h * vec_per_head;
-        const size_t dst = (((size_t)b * H_kv + h) * cap + pos) * d_h + c * 8;
+        const size_t dst = (base + h * hstride) * d_h + c * 8;
         *reinterpret_cast<uint4*>(kc + dst) = kr[j];
         *reinterpret_cast<uint4*>(vc + dst) = vr[j];
       }
@@ -232,7 +245,24 @@ extern "C" int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths, cons
   return launch_ex(kv_append_kernel, dim3(B), dim3(kKvThreads), 0, static_cast<cudaStream_t>(stream), 1,
                    static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths,
                    static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), src_ld, H_kv, cap, d_h,
-                   err_flag);
+                   err_flag, static_cast<const int32_t*>(nullptr), (int64_t)0, 0);
+}
+
+extern "C" int ps_kv_append_paged(void* k_pool, void* v_pool, int page_rows, const int32_t* block_table,
+                                  int64_t table_ld, int32_t* lengths, const void* k_new, const void* v_new,
+                                  int64_t src_ld, int B, int H_kv, int d_h, int32_t* err_flag, void* stream) {
+  if (B < 1 || H_kv < 1 || page_rows < 1 || table_ld < 1 || d_h < 8 || d_h % 8 || src_ld < (int64_t)H_kv * d_h ||
+      src_ld % 8)
+    return PS_ERR_VALUE;
+  if (!k_pool || !v_pool || !block_table || !lengths || !k_new || !v_new) return PS_ERR_VALUE;
+  if (((uintptr_t)k_new % 16) || ((uintptr_t)v_new % 16) || ((uintptr_t)k_pool % 16) || ((uintptr_t)v_pool % 16))
+    return PS_ERR_VALUE;
+  const long long cap = (long long)table_ld * page_rows;
+  if (cap >= (1ll << 31)) return PS_ERR_VALUE;
+  return launch_ex(kv_append_kernel, dim3(B), dim3(kKvThreads), 0, static_cast<cudaStream_t>(stream), 1,
+                   static_cast<uint16_t*>(k_pool), static_cast<uint16_t*>(v_pool), lengths,
+                   static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), src_ld, H_kv, (int)cap,
+                   d_h, err_flag, block_table, table_ld, page_rows);
 }
 
 static int ln_launch(float* x, int64_t x_ld, const float* add, const float* gamma, const float* beta, int B, int d,

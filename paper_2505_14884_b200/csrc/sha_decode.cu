@@ -59,6 +59,13 @@ struct ShaParams {
   const int32_t* sel;
   int group_base;
   int B, H, H_kv, cap, top_k;
+  // paged KV (ps_sha_decode_paged): logical row r of sequence b lives in
+  // physical page table[b * table_ld + r / page_rows], row r % page_rows, of
+  // a (pages, H_kv, page_rows, d_h) pool; NULL = contiguous (B, H_kv, cap, d_h)
+  const int32_t* table;
+  int64_t table_ld;
+  int page_rows;
+  int pool_pages;
   int NT;        // virtual tiles per unit (>= ceil(max length / T))
   int n_ctas;    // stream-K CTAs (the B zero-fill CTAs follow them)
   int max_seg;   // partial slots per unit
@@ -67,6 +74,52 @@ struct ShaParams {
   int64_t out_ld;
   int* counters;
   float* partials;
+};
+
+// Physical row of logical row `row0` of unit (b, g) in the row view of the
+// cache: (b*H_kv + g)*cap + row0 (contiguous) or (page*H_kv + g)*page_rows +
+// row0 % page_rows (paged).  The producer walks a unit's tiles in order: the
+// table entries of the first page and the next one are loaded when the unit
+// is entered (independent of the length load), and entering a page loads
+// the entry after it, so a table read is one page ahead of its use.
+struct PageCursor {
+  int b, g, pg, pb, pbn, off, base;
+  PS_DEV int entry(const ShaParams& p, int j) const {
+    return j < p.table_ld ? __ldg(p.table + (size_t)b * p.table_ld + j) : 0;
+  }
+  // issued before the unit's selection load so the two latencies overlap
+  PS_DEV void start(const ShaParams& p, int b_, int row_first) {
+    b = b_;
+    off = row_first;
+    if (p.table) {
+      pg = row_first / p.page_rows;
+      off = row_first - pg * p.page_rows;
+      pb = entry(p, pg);
+      pbn = entry(p, pg + 1);
+    }
+  }
+  PS_DEV void set_group(const ShaParams& p, int g_) {
+    g = g_;
+    base = (b * p.H_kv + g) * p.cap;  // contiguous slab of (b, g); rows < 2^31 (host-checked)
+  }
+  // physical row of the unit's next tile (tiles are consumed in order), then
+  // advance by `rows`: one add per tile, a table step per page
+  PS_DEV int next(const ShaParams& p, int rows) {
+    int r;
+    if (!p.table) {
+      r = base + off;
+    } else {
+      if (off == p.page_rows) {
+        pb = pbn;
+        ++pg;
+        pbn = entry(p, pg + 1);
+        off = 0;
+      }
+      r = (pb * p.H_kv + g) * p.page_rows + off;
+    }
+    off += rows;
+    return r;
+  }
 };
 
 template <int D_H, int G>
@@ -156,18 +209,16 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   struct Cursor {
     int u, t, len;
     bool live;
-    const uint16_t* kb;
-    const uint16_t* vb;
+    PageCursor pc;
   } cur;
   auto load_unit = [&](int u) {
     cur.u = u;
     const int b = u / p.top_k;
+    cur.pc.start(p, b, cur.t * S::T);
     const int g = (u == u_first ? sel_first : __ldg(p.sel + u)) - p.group_base;
     cur.live = g >= 0 && g < p.H_kv;
     cur.len = u == u_first ? len_first : __ldg(p.lengths + b);
-    const size_t slab = ((size_t)b * p.H_kv + (cur.live ? g : 0)) * (size_t)p.cap * D_H;
-    cur.kb = p.k + slab;
-    cur.vb = p.v + slab;
+    cur.pc.set_group(p, cur.live ? g : 0);
   };
   auto issue_next = [&](int stage) {
     const int row0 = cur.t * S::T;
@@ -176,9 +227,10 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
     } else {
       const int rows = min(S::T, cur.len - row0);
       const uint32_t bytes = (uint32_t)rows * D_H * 2;
+      const size_t off = (size_t)cur.pc.next(p, S::T) * D_H;
       mbar_arrive_expect_tx(&bars[stage], 2 * bytes);
-      bulk_g2s(sK + stage * S::T * D_H, cur.kb + (size_t)row0 * D_H, bytes, &bars[stage]);
-      bulk_g2s(sV + stage * S::T * D_H, cur.vb + (size_t)row0 * D_H, bytes, &bars[stage]);
+      bulk_g2s(sK + stage * S::T * D_H, p.k + off, bytes, &bars[stage]);
+      bulk_g2s(sV + stage * S::T * D_H, p.v + off, bytes, &bars[stage]);
     }
     if (++cur.t == p.NT) {  // advance the cursor
       cur.t = 0;
@@ -187,8 +239,8 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   };
   if (tid == 0 && n_it > 0) {
     const int u0 = (int)(f0 / p.NT);
-    load_unit(u0);
     cur.t = (int)(f0 - (long long)u0 * p.NT);
+    load_unit(u0);
     const int pre = min(kStages, n_it);
     for (int s2 = 0; s2 < pre; ++s2) issue_next(s2);
   }
@@ -504,29 +556,32 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
 
   // producer cursor (thread 0)
   struct Cursor {
-    int u, t, len, row_base;
+    int u, t, len;
     bool live;
+    PageCursor pc;
   } cur;
   auto load_unit = [&](int u) {
     cur.u = u;
     const int b = u / p.top_k;
+    cur.pc.start(p, b, cur.t * kMmaT);
     const int g = (u == u_first ? sel_first : __ldg(p.sel + u)) - p.group_base;
     cur.live = g >= 0 && g < p.H_kv;
     cur.len = u == u_first ? len_first : __ldg(p.lengths + b);
-    cur.row_base = (b * p.H_kv + (cur.live ? g : 0)) * p.cap;
+    cur.pc.set_group(p, cur.live ? g : 0);
   };
   auto issue_next = [&](int stage) {
     const int row0 = cur.t * kMmaT;
     if (!cur.live || row0 >= cur.len) {
       mbar_arrive(&bars[stage]);
     } else {
+      const int row = cur.pc.next(p, kMmaT);
       mbar_arrive_expect_tx(&bars[stage], 2 * kMmaTileBytes);
       uint8_t* k_dst = sK + stage * kMmaTileBytes;
       uint8_t* v_dst = sV + stage * kMmaTileBytes;
-      tma_load_2d(k_dst, &tmK, 0, cur.row_base + row0, &bars[stage]);
-      tma_load_2d(k_dst + 4096, &tmK, 64, cur.row_base + row0, &bars[stage]);
-      tma_load_2d(v_dst, &tmV, 0, cur.row_base + row0, &bars[stage]);
-      tma_load_2d(v_dst + 4096, &tmV, 64, cur.row_base + row0, &bars[stage]);
+      tma_load_2d(k_dst, &tmK, 0, row, &bars[stage]);
+      tma_load_2d(k_dst + 4096, &tmK, 64, row, &bars[stage]);
+      tma_load_2d(v_dst, &tmV, 0, row, &bars[stage]);
+      tma_load_2d(v_dst + 4096, &tmV, 64, row, &bars[stage]);
     }
     if (++cur.t == p.NT) {
       cur.t = 0;
@@ -534,8 +589,8 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
     }
   };
   if (tid == 0 && n_it > 0) {
-    load_unit(u_first);
     cur.t = (int)(f0 - (long long)u_first * p.NT);
+    load_unit(u_first);
     const int pre = min(kMmaStages, n_it);
     for (int s2 = 0; s2 < pre; ++s2) issue_next(s2);
   }
@@ -756,7 +811,8 @@ int launch_sha_mma(const ShaParams& prm, int grid, cudaStream_t st) {
       return PS_ERR_CUDA;
     configured = true;
   }
-  const uint64_t rows = (uint64_t)prm.B * prm.H_kv * prm.cap;
+  const uint64_t rows = prm.table ? (uint64_t)prm.pool_pages * prm.H_kv * prm.page_rows
+                                  : (uint64_t)prm.B * prm.H_kv * prm.cap;
   CUtensorMap tk, tv;
   int rc = sha_tmap(&tk, prm.k, rows);
   if (rc == PS_OK) rc = sha_tmap(&tv, prm.v, rows);
@@ -866,11 +922,11 @@ extern "C" int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_l
   return 0;
 }
 
-extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, const void* v_cache,
-                             const int32_t* lengths, const int32_t* sel, int group_base, int B, int H, int H_kv,
-                             int cap,
-                             int d_h, int top_k, float scale, int num_splits, int max_len_hint, void* out,
-                             int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
+static int sha_decode_impl(const void* q, int64_t q_ld, const void* k_cache, const void* v_cache,
+                           const int32_t* lengths, const int32_t* sel, int group_base, int B, int H, int H_kv,
+                           int cap, int d_h, int top_k, float scale, int num_splits, int max_len_hint, void* out,
+                           int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes, void* stream,
+                           const int32_t* table, int64_t table_ld, int page_rows, int pool_pages) {
   if (B < 1 || H < 1 || H_kv < 1 || cap < 1 || top_k < 1 || group_base < 0) return PS_ERR_VALUE;
   if (H % H_kv) return PS_ERR_VALUE;
   if ((int64_t)B * top_k > kMaxUnits) return PS_ERR_UNSUPPORTED;
@@ -897,6 +953,12 @@ extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, c
   prm.sel = sel;
   prm.group_base = group_base;
   prm.B = B; prm.H = H; prm.H_kv = H_kv; prm.cap = cap; prm.top_k = top_k;
+  prm.table = table;
+  prm.table_ld = table_ld;
+  prm.page_rows = table ? page_rows : cap;
+  prm.pool_pages = pool_pages;
+  if (table && page_rows % T) return PS_ERR_VALUE;  // a tile never straddles a page
+  if (!table && (long long)B * H_kv * cap >= (1ll << 31)) return PS_ERR_UNSUPPORTED;  // 32-bit row index
   prm.NT = NT;
   prm.n_ctas = sha_ctas(units, NT, num_splits);
   prm.max_seg = sha_max_seg(units, prm.n_ctas);
@@ -927,4 +989,28 @@ extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, c
     case 256: return dispatch_g<256>(prm, grid, G, bf16, st);
     default: return PS_ERR_UNSUPPORTED;
   }
+}
+
+extern "C" int ps_sha_decode(const void* q, int64_t q_ld, const void* k_cache, const void* v_cache,
+                             const int32_t* lengths, const int32_t* sel, int group_base, int B, int H, int H_kv,
+                             int cap,
+                             int d_h, int top_k, float scale, int num_splits, int max_len_hint, void* out,
+                             int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes, void* stream) {
+  return sha_decode_impl(q, q_ld, k_cache, v_cache, lengths, sel, group_base, B, H, H_kv, cap, d_h, top_k, scale,
+                         num_splits, max_len_hint, out, out_ld, out_dtype, ws, ws_bytes, stream, nullptr, 0, 0, 0);
+}
+
+extern "C" int ps_sha_decode_paged(const void* q, int64_t q_ld, const void* k_pool, const void* v_pool,
+                                   int pool_pages, int page_rows, const int32_t* block_table, int64_t table_ld,
+                                   const int32_t* lengths, const int32_t* sel, int group_base, int B, int H,
+                                   int H_kv, int d_h, int top_k, float scale, int num_splits, int max_len_hint,
+                                   void* out, int64_t out_ld, int out_dtype, void* ws, size_t ws_bytes,
+                                   void* stream) {
+  if (!block_table || pool_pages < 1 || page_rows < 1 || table_ld < 1) return PS_ERR_VALUE;
+  if ((long long)pool_pages * H_kv * page_rows >= (1ll << 31)) return PS_ERR_UNSUPPORTED;  // TMA row coordinate
+  const long long cap = (long long)table_ld * page_rows;
+  if (cap >= (1ll << 31)) return PS_ERR_VALUE;
+  return sha_decode_impl(q, q_ld, k_pool, v_pool, lengths, sel, group_base, B, H, H_kv, (int)cap, d_h, top_k,
+                         scale, num_splits, max_len_hint, out, out_ld, out_dtype, ws, ws_bytes, stream, block_table,
+                         table_ld, page_rows, pool_pages);
 }

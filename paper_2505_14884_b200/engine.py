@@ -18,6 +18,7 @@ replicated, all-reduce after the O- and down-projections) lives in
 
 from __future__ import annotations
 
+import copy
 import math
 from dataclasses import dataclass
 
@@ -28,7 +29,7 @@ from . import _lib, _ws
 from .exceptions import CapacityError, ConfigurationError
 from .kernels import ROW_PAD, _round_up, gather_gemm_into, mlp_into, sha_decode_into, swiglu_into
 from .model import DeviceModel, TransformerConfig
-from .tensors import KVCache
+from .tensors import KVCache, PagedKVCache
 from .validation import check_choice, check_count
 
 _MODES = ("dense", "dejavu_mlp", "polar")
@@ -87,7 +88,7 @@ class DecodeEngine:
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
                  caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
-                 concurrent_router: bool = False):
+                 concurrent_router: bool = False, kv_page_rows: int = 0):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
@@ -141,17 +142,31 @@ class DecodeEngine:
                 raise ValueError("caches must hold one KVCache per layer")
             self.caches = list(caches)
             ring = 0
-        base = [KVCache(batch, self.Hkv_loc, capacity, d_h, device=dev) for _ in range(ring)]
+        # kv_page_rows > 0: paged caches (block table per sequence, pages
+        # reserved for the whole capacity in a scattered order)
+        self.kv_page_rows = int(kv_page_rows)
+        if self.kv_page_rows and tp is not None:
+            raise ValueError("paged KV caches are not wired into tensor parallelism")
+
+        def new_cache(i):
+            if self.kv_page_rows:
+                pc = PagedKVCache(batch, self.Hkv_loc, capacity, d_h, page_rows=self.kv_page_rows, device=dev,
+                                  seed=1000 + i)
+                pc.reserve_all()
+                return pc
+            return KVCache(batch, self.Hkv_loc, capacity, d_h, device=dev)
+
+        base = [new_cache(i) for i in range(ring)]
         for ell in range(cfg.layers if ring else 0):
             c = base[ell % ring]
-            if ell >= ring:
-                alias = KVCache.__new__(KVCache)
-                alias.keys, alias.values = c.keys, c.values
+            if ell >= ring:  # shares the storage (and page table), own lengths
+                alias = copy.copy(c)
                 alias.lengths = torch.zeros(batch, dtype=torch.int32, device=dev)
                 alias.host_lengths = np.zeros(batch, dtype=np.int64)
                 alias._err = torch.zeros(1, dtype=torch.int32, device=dev)
                 c = alias
             self.caches.append(c)
+        self.paged = isinstance(self.caches[0], PagedKVCache)
         # static activation buffers (graph-capturable)
         f32, bf = torch.float32, torch.bfloat16
         D = cfg.ffn_dim
@@ -308,14 +323,23 @@ class DecodeEngine:
             n += self._linear_bf16(self.h, lw.w_qkv_t, lw.b_qkv, self.qkv, tag="gg_qkv")
             kq = self.qkv[:, self.d_loc:]
             vq = self.qkv[:, self.d_loc + self.dk_loc:]
-            if not k_h or self.concurrent_router:
+            if not k_h or self.concurrent_router or self.paged:
                 st = _lib.stream_ptr()
-                _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths), _lib.ptr(kq),
-                                          _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity, cfg.head_dim,
-                                          _lib.ptr(c._err), st), "ps_kv_append")
+                if self.paged:
+                    _lib.check(L.ps_kv_append_paged(_lib.ptr(c.k_pool), _lib.ptr(c.v_pool), c.page_rows,
+                                                    _lib.ptr(c.block_table), c.max_pages, _lib.ptr(c.lengths),
+                                                    _lib.ptr(kq), _lib.ptr(vq), qkv_w, B, self.Hkv_loc, cfg.head_dim,
+                                                    _lib.ptr(c._err), st), "ps_kv_append_paged")
+                else:
+                    _lib.check(L.ps_kv_append(_lib.ptr(c.keys), _lib.ptr(c.values), _lib.ptr(c.lengths),
+                                              _lib.ptr(kq), _lib.ptr(vq), qkv_w, B, self.Hkv_loc, c.capacity,
+                                              cfg.head_dim, _lib.ptr(c._err), st), "ps_kv_append")
                 n += 1
             if k_h and self.concurrent_router:
                 torch.cuda.current_stream().wait_stream(self.side)
+            elif k_h and self.paged:  # the fused head-router append writes contiguous caches only
+                sel = self._head_select(ell, k_h)
+                n += 1
             elif k_h:
                 # head router + top-k fused with the KV append (one launch)
                 sel = self._head_select(ell, k_h, append=(c, kq, vq, qkv_w))

@@ -24,7 +24,7 @@ import torch
 
 from . import _lib, _ws
 from .exceptions import EmptyCacheError
-from .tensors import KVCache, _rows_topk
+from .tensors import KVCache, PagedKVCache, _rows_topk
 from .validation import as_device_tensor, as_index_tensor, check_choice, check_count
 
 _ACTIVATIONS = ("none", "relu")
@@ -158,11 +158,12 @@ class FlashBlockParams:
 # Select-Head Attention
 # ---------------------------------------------------------------------------
 
-def sha_decode_into(q2d: torch.Tensor, q_ld: int, cache: KVCache, sel: torch.Tensor, n_heads: int,
+def sha_decode_into(q2d: torch.Tensor, q_ld: int, cache, sel: torch.Tensor, n_heads: int,
                     scale: float, out: torch.Tensor, out_ld: int, group_base: int = 0,
                     num_splits: int = 0, max_len_hint: int = 0) -> None:
-    """Raw launch (no validation) used by the engine's captured step."""
-    B, H_kv, cap, d_h = cache.keys.shape
+    """Raw launch (no validation) used by the engine's captured step;
+    ``cache`` is a KVCache or a PagedKVCache."""
+    B, H_kv, cap, d_h = cache.batch, cache.kv_heads, cache.capacity, cache.head_dim
     k = sel.shape[1]
     lib = _lib.load()
     if num_splits == 0:
@@ -170,6 +171,13 @@ def sha_decode_into(q2d: torch.Tensor, q_ld: int, cache: KVCache, sel: torch.Ten
     nbytes = lib.ps_sha_workspace_bytes(B, n_heads, H_kv, d_h, k, num_splits)
     ws = _ws.get("sha", nbytes, cache.device)
     dt = _lib.PS_DTYPE_BF16 if out.dtype == torch.bfloat16 else _lib.PS_DTYPE_F32
+    if isinstance(cache, PagedKVCache):
+        _lib.call("ps_sha_decode_paged", _lib.ptr(q2d), int(q_ld), _lib.ptr(cache.k_pool), _lib.ptr(cache.v_pool),
+                  cache.pool_pages, cache.page_rows, _lib.ptr(cache.block_table), cache.max_pages,
+                  _lib.ptr(cache.lengths), _lib.ptr(sel), int(group_base), B, n_heads, H_kv, d_h, k,
+                  float(scale), int(num_splits), int(max_len_hint), _lib.ptr(out), int(out_ld), dt,
+                  _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        return
     _lib.call("ps_sha_decode", _lib.ptr(q2d), int(q_ld), _lib.ptr(cache.keys), _lib.ptr(cache.values),
               _lib.ptr(cache.lengths), _lib.ptr(sel), int(group_base), B, n_heads, H_kv, cap, d_h, k,
               float(scale), int(num_splits), int(max_len_hint), _lib.ptr(out), int(out_ld), dt,
@@ -183,7 +191,8 @@ def _check_attention_args(q, cache: KVCache, bhi: BatchHeadIndex, scale):
         raise ValueError(f"q must have a singleton query axis (B, H, 1, d_h), got {tuple(q4.shape)}")
     batch, _, _, d_h = q4.shape
     if cache.batch != batch or cache.head_dim != d_h:
-        raise ValueError(f"cache shape {tuple(cache.keys.shape)} inconsistent with query {tuple(q4.shape)}")
+        raise ValueError(f"cache shape {(cache.batch, cache.kv_heads, cache.capacity, cache.head_dim)} "
+                         f"inconsistent with query {tuple(q4.shape)}")
     if bhi.batch != batch:
         raise ValueError(f"batch_head_index covers {bhi.batch} sequences, not {batch}")
     if (cache.host_lengths < 1).any():

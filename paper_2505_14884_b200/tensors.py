@@ -191,6 +191,213 @@ class KVCache:
         return self.values[b, h, : int(self.host_lengths[b])]
 
 
+class PagedKVCache:
+    """Block-table KV cache with the ``KVCache`` API.
+
+    The reference cache is one contiguous (B, H_kv, cap, d_h) array
+    (tensors.py:116-213).  Here K/V live in page pools of layout
+    (pages, H_kv, page_rows, d_h) bf16 and ``block_table`` (B, max_pages)
+    int32 maps sequence b's logical rows [j*page_rows, (j+1)*page_rows) to
+    a physical page -- the serving format (pages are allocated as sequences
+    grow and returned by :meth:`release`).  The SHA kernel streams the same
+    32-row tiles through the table (``ps_sha_decode_paged``); ``page_rows``
+    must be a multiple of the tile (4096 / head_dim rows).
+    """
+
+    def __init__(self, batch: int, kv_heads: int, capacity: int, head_dim: int, page_rows: int = 64,
+                 pool_pages: int | None = None, device="cuda", dtype=torch.bfloat16, seed: int | None = None):
+        check_count(batch, "batch")
+        check_count(kv_heads, "kv_heads")
+        check_count(capacity, "capacity")
+        check_count(head_dim, "head_dim")
+        check_count(page_rows, "page_rows")
+        if dtype != torch.bfloat16:
+            raise ValueError("the B200 cache stores bf16 K/V")
+        tile = max(1, 4096 // head_dim)
+        if page_rows % tile:
+            raise ValueError(f"page_rows must be a multiple of the SHA tile ({tile} rows at head_dim {head_dim})")
+        self.page_rows = page_rows
+        self.max_pages = -(-capacity // page_rows)
+        pool = pool_pages if pool_pages is not None else batch * self.max_pages
+        check_count(pool, "pool_pages")
+        shape = (pool, kv_heads, page_rows, head_dim)
+        self.k_pool = torch.zeros(shape, dtype=dtype, device=device)
+        self.v_pool = torch.zeros(shape, dtype=dtype, device=device)
+        self.block_table = torch.zeros((batch, self.max_pages), dtype=torch.int32, device=device)
+        self.host_table = np.full((batch, self.max_pages), -1, dtype=np.int64)
+        self.lengths = torch.zeros(batch, dtype=torch.int32, device=device)
+        self.host_lengths = np.zeros(batch, dtype=np.int64)
+        self._err = torch.zeros(1, dtype=torch.int32, device=device)
+        order = np.arange(pool)
+        if seed is not None:  # scattered page placement (tests / benchmarks)
+            np.random.default_rng(seed).shuffle(order)
+        self._free = list(order[::-1])
+        self._batch, self._kv_heads, self._head_dim = batch, kv_heads, head_dim
+
+    # KVCache-compatible shape API
+    @property
+    def batch(self) -> int:
+        return self._batch
+
+    @property
+    def kv_heads(self) -> int:
+        return self._kv_heads
+
+    @property
+    def capacity(self) -> int:
+        return self.max_pages * self.page_rows
+
+    @property
+    def head_dim(self) -> int:
+        return self._head_dim
+
+    @property
+    def pool_pages(self) -> int:
+        return self.k_pool.shape[0]
+
+    @property
+    def device(self):
+        return self.k_pool.device
+
+    def _sync_lengths(self) -> None:
+        self.lengths.copy_(torch.from_numpy(self.host_lengths.astype(np.int32)))
+
+    # ------------------------------------------------------------ page management
+    def reserve(self, b: int, rows: int) -> None:
+        """Map pages so sequence b can hold ``rows`` rows (host allocator,
+        one H2D copy of the changed table row)."""
+        need = -(-int(rows) // self.page_rows)
+        if need > self.max_pages:
+            raise CapacityError(f"sequence {b}: {rows} rows exceed capacity {self.capacity}")
+        row = self.host_table[b]
+        changed = False
+        for j in range(need):
+            if row[j] < 0:
+                if not self._free:
+                    raise CapacityError("KV page pool exhausted")
+                row[j] = self._free.pop()
+                changed = True
+        if changed:
+            self.block_table[b].copy_(torch.from_numpy(np.maximum(row, 0).astype(np.int32)))
+
+    def reserve_all(self) -> None:
+        for b in range(self.batch):
+            self.reserve(b, self.capacity)
+
+    def release(self, b: int) -> None:
+        """Return sequence b's pages to the pool and empty it."""
+        row = self.host_table[b]
+        self._free.extend(int(p) for p in row[row >= 0][::-1])
+        row[:] = -1
+        self.block_table[b].zero_()
+        self.host_lengths[b] = 0
+        self._sync_lengths()
+
+    def _page_rows_of(self, b: int, start: int, stop: int):
+        """(page, row-in-page, logical start, logical stop) runs covering [start, stop)."""
+        P = self.page_rows
+        r = start
+        while r < stop:
+            j, o = divmod(r, P)
+            e = min(stop, (j + 1) * P)
+            yield int(self.host_table[b, j]), o, r, e
+            r = e
+
+    # ------------------------------------------------------------ KVCache API
+    def append_step(self, k_new, v_new, src_ld=None) -> None:
+        """tensors.py:150-170 into the page holding each sequence's next row."""
+        if (self.host_lengths >= self.capacity).any():
+            raise CapacityError(f"KV cache capacity {self.capacity} exhausted")
+        for b in range(self.batch):
+            self.reserve(b, int(self.host_lengths[b]) + 1)
+        k_new = as_device_tensor(k_new, "k_new", dtype=torch.bfloat16)
+        v_new = as_device_tensor(v_new, "v_new", dtype=torch.bfloat16)
+        if src_ld is None:
+            expect = (self.batch, self.kv_heads, self.head_dim)
+            if tuple(k_new.shape) != expect or tuple(v_new.shape) != expect:
+                raise ValueError(f"append_step expects shape {expect}")
+            k_new, v_new = k_new.contiguous(), v_new.contiguous()
+            src_ld = self.kv_heads * self.head_dim
+        _lib.call("ps_kv_append_paged", _lib.ptr(self.k_pool), _lib.ptr(self.v_pool), self.page_rows,
+                  _lib.ptr(self.block_table), self.max_pages, _lib.ptr(self.lengths), _lib.ptr(k_new),
+                  _lib.ptr(v_new), int(src_ld), self.batch, self.kv_heads, self.head_dim, _lib.ptr(self._err),
+                  _lib.stream_ptr())
+        self.host_lengths += 1
+
+    def append_tokens(self, b: int, k_tokens, v_tokens) -> None:
+        """tensors.py:172-192 -- a run of tokens for one sequence (prefill)."""
+        k_tokens = as_device_tensor(k_tokens, "k_tokens", dtype=torch.bfloat16, device=self.device)
+        v_tokens = as_device_tensor(v_tokens, "v_tokens", dtype=torch.bfloat16, device=self.device)
+        t = k_tokens.shape[0]
+        if tuple(k_tokens.shape[1:]) != (self.kv_heads, self.head_dim):
+            raise ValueError("k_tokens shape mismatch with cache")
+        start = int(self.host_lengths[b])
+        if start + t > self.capacity:
+            raise CapacityError(f"sequence {b}: {start}+{t} tokens exceed capacity {self.capacity}")
+        self.reserve(b, start + t)
+        for pg, o, r0, r1 in self._page_rows_of(b, start, start + t):
+            self.k_pool[pg, :, o:o + r1 - r0] = k_tokens[r0 - start:r1 - start].transpose(0, 1)
+            self.v_pool[pg, :, o:o + r1 - r0] = v_tokens[r0 - start:r1 - start].transpose(0, 1)
+        self.host_lengths[b] = start + t
+        self._sync_lengths()
+
+    def set_lengths(self, lengths) -> None:
+        lengths = np.asarray(lengths, dtype=np.int64).reshape(self.batch)
+        if (lengths < 0).any() or (lengths > self.capacity).any():
+            raise ValueError("lengths out of range")
+        for b in range(self.batch):
+            self.reserve(b, int(lengths[b]))
+        self.host_lengths[:] = lengths
+        self._sync_lengths()
+
+    def load_contiguous(self, keys, values, lengths) -> None:
+        """Copy (B, H_kv, >= max length, d_h) K/V histories into pages."""
+        lengths = np.asarray(lengths, dtype=np.int64).reshape(self.batch)
+        for b in range(self.batch):
+            n = int(lengths[b])
+            if n > self.capacity:
+                raise CapacityError(f"sequence {b}: {n} rows exceed capacity {self.capacity}")
+            self.reserve(b, n)
+            for pg, o, r0, r1 in self._page_rows_of(b, 0, n):
+                self.k_pool[pg, :, o:o + r1 - r0] = keys[b, :, r0:r1]
+                self.v_pool[pg, :, o:o + r1 - r0] = values[b, :, r0:r1]
+        self.host_lengths[:] = lengths
+        self._sync_lengths()
+
+    @classmethod
+    def from_contiguous(cls, cache: "KVCache", page_rows: int = 64, pool_pages: int | None = None,
+                        seed: int | None = None) -> "PagedKVCache":
+        out = cls(cache.batch, cache.kv_heads, cache.capacity, cache.head_dim, page_rows=page_rows,
+                  pool_pages=pool_pages, device=cache.device, seed=seed)
+        out.load_contiguous(cache.keys, cache.values, cache.host_lengths)
+        return out
+
+    def fill_random(self, rng, length: int) -> None:
+        """tensors.py:201-213 -- same draws as ``KVCache.fill_random``."""
+        if not 1 <= length <= self.capacity:
+            raise ValueError(f"length must be in [1, {self.capacity}]")
+        shape = (self.batch, self.kv_heads, length, self.head_dim)
+        if isinstance(rng, np.random.Generator):
+            k = torch.from_numpy(rng.standard_normal(shape, dtype=np.float32)).to(self.device, torch.bfloat16)
+            v = torch.from_numpy(rng.standard_normal(shape, dtype=np.float32)).to(self.device, torch.bfloat16)
+        else:
+            gen = rng if isinstance(rng, torch.Generator) else None
+            if gen is None:
+                gen = torch.Generator(device=self.device)
+                gen.manual_seed(int(rng) if rng is not None else 0)
+            k = torch.empty(shape, dtype=torch.bfloat16, device=self.device).normal_(generator=gen)
+            v = torch.empty(shape, dtype=torch.bfloat16, device=self.device).normal_(generator=gen)
+        self.load_contiguous(k, v, np.full(self.batch, length))
+
+    def keys_for(self, b: int, h: int) -> torch.Tensor:
+        return torch.cat([self.k_pool[pg, h, o:o + r1 - r0]
+                          for pg, o, r0, r1 in self._page_rows_of(b, 0, int(self.host_lengths[b]))])
+
+    def values_for(self, b: int, h: int) -> torch.Tensor:
+        return torch.cat([self.v_pool[pg, h, o:o + r1 - r0]
+                          for pg, o, r0, r1 in self._page_rows_of(b, 0, int(self.host_lengths[b]))])
+
+
 def l2_norm_per_head(attn_out) -> torch.Tensor:
     """tensors.py:76-80 (study helper; plain torch on device)."""
     a = as_device_tensor(attn_out, "attn_out")

@@ -1,0 +1,147 @@
+"""Paged KV cache: SHA through a block table is
+bit-identical to SHA over the contiguous cache with the same contents (same
+tiles, same partition, same merge order), matches the oracle, never reads
+rows past a length or pages it does not map (NaN poison), and the paged
+append writes the same rows as the contiguous one."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import polar_oracle as po
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2505_14884_b200 as pb  # noqa: E402
+
+DEV = torch.device("cuda")
+
+
+def _t(a):
+    return torch.as_tensor(np.asarray(a, np.float32), device=DEV)
+
+
+@pytest.mark.parametrize("B,H,H_kv,d_h,N,P", [(6, 32, 32, 128, 300, 32), (5, 32, 8, 128, 700, 64),
+                                              (3, 64, 8, 128, 1000, 128), (4, 8, 8, 32, 400, 128),
+                                              (4, 8, 2, 64, 260, 64)])
+def test_paged_sha_equals_contiguous_and_oracle(B, H, H_kv, d_h, N, P):
+    rng = np.random.default_rng(B * 31 + H_kv + P)
+    c = pb.KVCache(B, H_kv, N + 40, d_h, device=DEV)
+    c.fill_random(rng, N)
+    lens = rng.integers(1, N + 1, size=B)
+    lens[0] = N
+    lens[-1] = 1
+    c.set_lengths(lens)
+    # scattered pages in a pool with spare pages
+    pc = pb.PagedKVCache.from_contiguous(c, page_rows=P, pool_pages=B * (-(-(N + 40) // P)) + 7, seed=5)
+    assert (pc.host_table[0][: -(-N // P)] >= 0).all()
+    q = po.round_bf16(rng.normal(size=(B, H, 1, d_h)).astype(np.float32))
+    k = max(1, H_kv // 2)
+    sel = np.stack([np.sort(rng.choice(H_kv, k, replace=False)) for _ in range(B)])
+    bhi = pb.BatchHeadIndex(sel)
+    ref_dev = pb.gqa_selective_attention_decode(_t(q), c, bhi).cpu()
+    got = pb.gqa_selective_attention_decode(_t(q), pc, bhi).cpu()
+    assert torch.equal(got, ref_dev)
+    ref = po.naive_attention_reference(q, c.keys.float().cpu().numpy(), c.values.float().cpu().numpy(), lens,
+                                       sel, H // H_kv)
+    assert np.abs(got.numpy() - ref).max() <= 1e-2
+    # poison: unmapped pages, rows past each length inside mapped pages, and
+    # non-selected groups -- none of it may be read
+    mapped = set(int(p) for p in pc.host_table[pc.host_table >= 0].ravel())
+    for pg in range(pc.pool_pages):
+        if pg not in mapped:
+            pc.k_pool[pg] = float("nan")
+            pc.v_pool[pg] = float("nan")
+    for b in range(B):
+        n = int(lens[b])
+        for j in range(pc.max_pages):
+            pg = int(pc.host_table[b, j])
+            if pg < 0:
+                continue
+            lo = max(0, n - j * P)
+            if lo < P:
+                pc.k_pool[pg, :, lo:] = float("nan")
+                pc.v_pool[pg, :, lo:] = float("nan")
+            for g in range(H_kv):
+                if g not in sel[b]:
+                    pc.k_pool[pg, g] = float("nan")
+                    pc.v_pool[pg, g] = float("nan")
+    poisoned = pb.gqa_selective_attention_decode(_t(q), pc, bhi).cpu()
+    assert torch.isfinite(poisoned).all()
+    assert torch.equal(poisoned, got)
+
+
+def test_paged_append_matches_contiguous():
+    rng = np.random.default_rng(3)
+    B, H_kv, d_h, P = 5, 4, 128, 32
+    c = pb.KVCache(B, H_kv, 130, d_h, device=DEV)
+    c.fill_random(rng, 30)
+    c.set_lengths([30, 31, 32, 63, 64])  # appends land mid-page, at page ends and on fresh pages
+    pc = pb.PagedKVCache.from_contiguous(c, page_rows=P, seed=1)
+    for _ in range(3):
+        kn = torch.randn(B, H_kv, d_h, device=DEV).bfloat16()
+        vn = torch.randn(B, H_kv, d_h, device=DEV).bfloat16()
+        c.append_step(kn, vn)
+        pc.append_step(kn, vn)
+    assert pc.lengths.cpu().tolist() == c.lengths.cpu().tolist() == [33, 34, 35, 66, 67]
+    for b in range(B):
+        for h in range(H_kv):
+            assert torch.equal(pc.keys_for(b, h), c.keys_for(b, h))
+            assert torch.equal(pc.values_for(b, h), c.values_for(b, h))
+    # a fused strided source (the engine's QKV buffer layout) works too
+    qkv = torch.randn(B, 3 * H_kv * d_h, device=DEV).bfloat16()
+    kq, vq = qkv[:, H_kv * d_h:], qkv[:, 2 * H_kv * d_h:]
+    pc.append_step(kq, vq, src_ld=qkv.stride(0))
+    assert torch.equal(pc.keys_for(2, 1)[-1], kq[2, d_h:2 * d_h])
+
+
+def test_paged_capacity_and_validation():
+    pc = pb.PagedKVCache(2, 2, 64, 128, page_rows=32, pool_pages=3, device=DEV)
+    pc.set_lengths([64, 0])
+    with pytest.raises(pb.CapacityError):  # pool exhausted
+        pc.set_lengths([64, 64])
+    pc.release(0)
+    pc.set_lengths([0, 64])
+    kn = torch.zeros(2, 2, 128, device=DEV).bfloat16()
+    with pytest.raises(pb.CapacityError):
+        pc.append_step(kn, kn)
+    with pytest.raises(ValueError):
+        pb.PagedKVCache(2, 2, 64, 128, page_rows=48, device=DEV)  # not a tile multiple
+
+
+@pytest.mark.parametrize("kv_heads,mode", [(8, "polar"), (2, "polar"), (8, "dense")])
+def test_engine_step_paged_equals_contiguous(kv_heads, mode):
+    """The decode engine over paged caches (scattered pages, separate paged
+    append) produces the contiguous engine's logits, eager and from the
+    captured graph."""
+    from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy
+    from paper_2505_14884_b200.model import DeviceModel, TransformerConfig
+
+    cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 288, "relu")
+    model = DeviceModel.from_host(cfg, po.random_model(2, 256, 1024, 8, kv_heads, 512, 288, seed=21))
+    polar = mode == "polar"
+    pol = SparsityPolicy(mode=mode, mlp_k_table={0: 128, 1: 128} if polar else None,
+                         head_density=0.5 if polar else 1.0)
+    hr = [pb.HeadRouter(256, kv_heads, seed=40 + e) for e in range(2)]
+    mr = [pb.MlpRouter(256, 1024, seed=30 + e) for e in range(2)]
+    engs = []
+    for pr in (0, 128):  # head_dim 32: the SHA tile is 128 rows
+        e = DecodeEngine(model, 8, 288, pol, head_routers=hr, mlp_routers=mr, kv_page_rows=pr)
+        rng = np.random.default_rng(22)
+        for c in e.caches:
+            c.fill_random(rng, 252)
+        engs.append(e)
+    assert engs[1].paged and not engs[0].paged
+    tokens = np.random.default_rng(1).integers(0, 512, 8)
+    for _ in range(2):
+        a, b = engs[0].step(tokens).clone(), engs[1].step(tokens).clone()
+        assert torch.equal(a, b)
+    engs[1].capture()
+    engs[0].capture()
+    for _ in range(3):  # crosses the 256-row page boundary (252 + 5 steps)
+        a, b = engs[0].step(tokens).clone(), engs[1].step(tokens).clone()
+        assert torch.equal(a, b)
+    assert engs[1].caches[1].lengths.cpu().tolist() == [257] * 8
