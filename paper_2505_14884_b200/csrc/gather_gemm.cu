@@ -32,6 +32,8 @@
 #include <type_traits>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ps {
@@ -68,6 +70,7 @@ struct GGParams {
   int64_t out_ld;
   int out_bf16;
   int vec_ok;  // out / residual rows 16-byte aligned: vector epilogue stores
+  int push;     // split-K reduction: 1 = partial rows pushed to their owner CTA (st.async), 0 = pulled (DSMEM loads)
   int a_early;  // A (weights, idx, count) ready before the previous kernel ends: stream A pre-griddep_wait
   unsigned long long* trace;  // debug: per-CTA timestamps (ps_debug_gemm_trace), NULL normally
 };
@@ -192,8 +195,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
       }
-      mbar_init(rdy, C);
-      mbar_init(fre, C);
+      mbar_init(rdy, p.push ? 1 : C);
+      mbar_init(fre, p.push ? (C > 1 ? C - 1 : 1) : C);
       fence_mbar_init();
     }
     __syncwarp();
@@ -465,6 +468,81 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_after();
       for (int cb = 0; cb < NB; cb += kEpiCols) {
         const int ncb = min(kEpiCols, NB - cb);
+        if (C > 1 && p.push) {
+          // ---- push reduction: CTA `rank` owns rows [rank*rows, (rank+1)*rows) of
+          // the tile.  Every CTA sends each row's partial straight from TMEM to
+          // the owner's slot `rank` (st.async, completing bytes on the owner's
+          // rdy barrier); the owner sums its C slots from local shared memory.
+          // stg is viewed as slot[C][kEpiCols][rows].
+          const int rows_o = rows;
+          const int rows_here = min(ncb, nrows - cb);
+          if (use > 0) mbar_wait_cluster(fre, (use - 1) & 1);  // every owner consumed the last chunk
+          {
+            const int o = m / rows_o, ml = m - o * rows_o;
+            const uint32_t dst = peer_stg[o], bar_o = peer_rdy[o];
+            for (int c0 = 0; c0 < ncb; c0 += 16) {
+              uint32_t r[16];
+              if (nkb > 0) {
+                tmem_ld16(tmem + a * NB + ((uint32_t)(q * 32) << 16) + cb + c0, r);
+                tmem_ld_wait();
+              } else {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) r[u] = 0u;
+              }
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int idx = (rank * kEpiCols + c0 + u) * rows_o + ml;
+                if (o == rank) stg[idx] = __uint_as_float(r[u]);
+                else st_async_f32(dst + (uint32_t)idx * 4u, __uint_as_float(r[u]), bar_o);
+              }
+            }
+          }
+          if (cb + kEpiCols >= NB) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);  // accumulator free for the MMA warp
+          }
+          if (et == 0) mbar_arrive_expect_tx(rdy, (uint32_t)((C - 1) * rows_o * ncb * 4));
+          auto push_reduce = [&](auto cc) {
+            constexpr int CC = decltype(cc)::value;
+            constexpr int NV = (kEpiCols * (BM / CC / 4)) / kEpiThreads;  // vectors per thread
+            const int vpn = BM / CC / 4;
+            const int mloc = (et % vpn) * 4;
+            float4 res[NV];
+#pragma unroll
+            for (int g = 0; g < NV; ++g) {  // residual rows in flight across the wait
+              const int v = et + g * kEpiThreads;
+              res[g] = v < rows_here * vpn ? load_res(cb + v / vpn) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));  // my own slot written
+            mbar_wait_cluster(rdy, use & 1);                      // the peers' slots landed
+            if (tr && et == 0 && j == 0 && cb == 0) tr[11] = gtimer();
+#pragma unroll
+            for (int g = 0; g < NV; ++g) {
+              const int v = et + g * kEpiThreads;
+              if (v < rows_here * vpn) {
+                const int n = v / vpn;
+                float4 sum = *reinterpret_cast<const float4*>(stg + n * rows_o + mloc);
+#pragma unroll
+                for (int c = 1; c < CC; ++c) {
+                  const float4 t4 = *reinterpret_cast<const float4*>(stg + (c * kEpiCols + n) * rows_o + mloc);
+                  sum.x += t4.x; sum.y += t4.y; sum.z += t4.z; sum.w += t4.w;
+                }
+                finish4r(cb + n, sum, res[g]);
+              }
+            }
+          };
+          if (C == 2) push_reduce(std::integral_constant<int, 2>{});
+          else if (C == 4) push_reduce(std::integral_constant<int, 4>{});
+          else push_reduce(std::integral_constant<int, 8>{});
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads));  // every read of my slots done
+          if (tr && et == 0 && j == 0 && cb == 0) tr[12] = gtimer();
+          if (et == 0 && !(j == my_tiles - 1 && cb + kEpiCols >= NB))
+            for (int c = 0; c < C; ++c)
+              if (c != rank) remote_arrive_relaxed(peer_fre[c]);
+          ++use;
+          continue;
+        }
         // 1) this CTA's partial (or zero) -> staging tile stg[n][m]
         for (int c0 = 0; c0 < ncb; c0 += 16) {
           uint32_t r[16];
@@ -566,6 +644,7 @@ int pick_nb(int N) {
 
 unsigned long long* g_trace = nullptr;
 int g_stages_override = 0, g_target_override = 0;
+int g_push = -1;     // -1: from env PS_GG_PUSH (default 1)
 int g_lsu_mode = 1;  // 0: TMA for A, 1: LSU for gathered A, 2: LSU for all A
 
 int ctas_per_sm(int NB) { return NB <= 128 ? 2 : 1; }
@@ -708,6 +787,11 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
   prm.out_ld = out_ld;
   prm.out_bf16 = out_dtype == PS_DTYPE_BF16;
   prm.a_early = 0;
+  if (g_push < 0) {
+    const char* e = getenv("PS_GG_PUSH");
+    g_push = e ? atoi(e) : 1;
+  }
+  prm.push = g_push;
   prm.vec_ok = (out_ld % 4 == 0) && ((uintptr_t)out % 16 == 0);
   return PS_OK;
 }
