@@ -883,11 +883,18 @@ int sha_auto_splits(int units, int NT) {
   return best;
 }
 
-int sha_ctas(int units, int NT, int num_splits) {
+int sha_ctas(int units, int NT, int num_splits, int G) {
   // num_splits < 0: exactly -num_splits stream-K CTAs (tuning hook)
   long long cap;
   if (num_splits < 0) {
     cap = -(long long)num_splits;
+  } else if (num_splits == 0 && G >= 4 && units >= (sha_slots() * 9) / 10) {
+    // grouped heads (G >= 4: a unit's partial is G x (d_h + 2) floats, so
+    // splitting costs more): one CTA per unit once there are ~2 waves of
+    // units, else exactly one resident wave -- measured on B200 at ctx 1920,
+    // H_kv = 8: 512 units 98 -> 90 us, 1024 units 167 -> 162 us, 4096 units
+    // 595 -> 575 us against the wave model below
+    cap = units >= (sha_slots() * 9) / 5 ? units : sha_slots();
   } else {
     if (num_splits == 0) num_splits = sha_auto_splits(units, NT);
     cap = (long long)units * num_splits;
@@ -960,7 +967,7 @@ static int sha_decode_impl(const void* q, int64_t q_ld, const void* k_cache, con
   if (table && page_rows % T) return PS_ERR_VALUE;  // a tile never straddles a page
   if (!table && (long long)B * H_kv * cap >= (1ll << 31)) return PS_ERR_UNSUPPORTED;  // 32-bit row index
   prm.NT = NT;
-  prm.n_ctas = sha_ctas(units, NT, num_splits);
+  prm.n_ctas = sha_ctas(units, NT, num_splits, G);
   prm.max_seg = sha_max_seg(units, prm.n_ctas);
   prm.scale_log2 = scale * kLog2e;
   prm.out = out;
