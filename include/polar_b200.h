@@ -212,6 +212,10 @@ void ps_debug_gemm_trace(void* buf, int stages, int target_ctas);
 /* A-operand copy engine: 0 = TMA (tile / tile::gather4), 1 = cp.async loader
  * warps for gathered rows (default), 2 = cp.async loader warps always */
 void ps_debug_gemm_lsu_mode(int mode);
+/* small-batch path of ps_gather_gemm: N <= 4 (and no residual) runs a
+ * CUDA-core gathered GEMV -- whole rows per warp, no split-K -- instead of the
+ * tcgen05 tiles; 0 forces the tiles (default 1, env PS_GG_GEMV) */
+void ps_debug_gemm_gemv(int enable);
 /* flags: PS_GG_A_READY -- w_rows, idx and count_dev were written at least
  * two launches earlier in the stream (or are static): the A stream may start
  * before the immediately preceding kernel completes (programmatic dependent

@@ -52,6 +52,7 @@ SIGNATURES = {
                                         _i64, _i, _i, _i, _vp, _vp]),
     "ps_debug_gemm_trace": (None, [_vp, _i, _i]),
     "ps_debug_gemm_lsu_mode": (None, [_i]),
+    "ps_debug_gemm_gemv": (None, [_i]),
     "ps_debug_topk_trace": (None, [_vp]),
     "ps_gather_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "ps_gather_gemm_auto_splits": (_i, [_i, _i, _i]),

@@ -796,6 +796,127 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
   return PS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Small-batch UP projection as a gathered GEMV on CUDA cores (N <= 4; at 8
+// and 16 rows the per-element x unpacking makes it FMA-bound and the tcgen05
+// tiles win -- measured in the decode step): every
+// warp owns whole rows (two at a time, sharing the x loads), so there is no
+// split-K and no cross-CTA reduction -- the kernel is a pure row stream.  x is
+// staged once per CTA in shared memory (rows >= N zero).  Positions in
+// [count, round_up(count, pad)) are written as zeros, like the tile path.
+constexpr int kGvThreads = 256;
+constexpr int kGvUnroll = 4;
+
+template <int NB>
+__global__ void __launch_bounds__(kGvThreads) gemv_up_kernel(const uint16_t* __restrict__ w, int64_t w_ld,
+                                                             const int32_t* __restrict__ idx,
+                                                             const int32_t* __restrict__ count_dev, int M,
+                                                             const uint16_t* __restrict__ x, int64_t x_ld, int N,
+                                                             int K, const float* __restrict__ bias, int act,
+                                                             void* out, int64_t out_ld, int out_bf16, int pad) {
+  extern __shared__ __align__(16) uint4 sx4[];  // [NB][K / 8]
+  const int kv = K >> 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_wait();  // x, idx and count come from the preceding kernels
+  griddep_launch();
+  const int count = count_dev ? min(__ldg(count_dev), M) : M;
+  for (int i = threadIdx.x; i < NB * kv; i += kGvThreads) {
+    const int b = i / kv, c = i - b * kv;
+    sx4[i] = b < N ? __ldg(reinterpret_cast<const uint4*>(x + (size_t)b * x_ld) + c) : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const int nw = gridDim.x * (kGvThreads / 32);
+  for (int p0 = 2 * (blockIdx.x * (kGvThreads / 32) + warp); p0 < count; p0 += 2 * nw) {
+    const bool two = p0 + 1 < count;
+    const int id0 = idx ? __ldg(idx + p0) : p0;
+    const int id1 = two ? (idx ? __ldg(idx + p0 + 1) : p0 + 1) : id0;
+    const uint4* w0 = reinterpret_cast<const uint4*>(w + (size_t)id0 * w_ld);
+    const uint4* w1 = reinterpret_cast<const uint4*>(w + (size_t)id1 * w_ld);
+    float acc0[NB], acc1[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
+    for (int c0 = lane; c0 < kv; c0 += 32 * kGvUnroll) {
+      uint4 a0[kGvUnroll], a1[kGvUnroll];
+#pragma unroll
+      for (int u = 0; u < kGvUnroll; ++u) {
+        const int c = c0 + 32 * u;
+        a0[u] = c < kv ? __ldg(w0 + c) : make_uint4(0, 0, 0, 0);
+        a1[u] = c < kv ? __ldg(w1 + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kGvUnroll; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < kv) {
+          float wa[8], wb[8];
+          unpack8(a0[u], wa);
+          unpack8(a1[u], wb);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            float xf[8];
+            unpack8(sx4[b * kv + c], xf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              acc0[b] = fmaf(wa[e], xf[e], acc0[b]);
+              acc1[b] = fmaf(wb[e], xf[e], acc1[b]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      acc0[b] = warp_sum(acc0[b]);
+      acc1[b] = warp_sum(acc1[b]);
+    }
+    // lane b stores batch row b of both positions
+    float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      if (lane == b) { v0 = acc0[b]; v1 = acc1[b]; }
+    if (lane < N) {
+      const float b0 = bias ? __ldg(bias + id0) : 0.f, b1 = bias ? __ldg(bias + id1) : 0.f;
+      v0 += b0;
+      v1 += b1;
+      if (act == PS_ACT_RELU) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
+      const size_t o = (size_t)lane * out_ld + p0;
+      if (out_bf16) {
+        reinterpret_cast<uint16_t*>(out)[o] = f2bf(v0);
+        if (two) reinterpret_cast<uint16_t*>(out)[o + 1] = f2bf(v1);
+      } else {
+        reinterpret_cast<float*>(out)[o] = v0;
+        if (two) reinterpret_cast<float*>(out)[o + 1] = v1;
+      }
+    }
+  }
+  // zero the padding positions the next kernel may read
+  const int pend = min((count + pad - 1) / pad * pad, (int)out_ld);
+  for (int i = blockIdx.x * kGvThreads + threadIdx.x; i < (pend - count) * N; i += gridDim.x * kGvThreads) {
+    const int b = i / (pend - count), pp = count + (i - b * (pend - count));
+    if (out_bf16) reinterpret_cast<uint16_t*>(out)[(size_t)b * out_ld + pp] = 0;
+    else reinterpret_cast<float*>(out)[(size_t)b * out_ld + pp] = 0.f;
+  }
+}
+
+int g_gemv = -1;  // -1: from env PS_GG_GEMV (default 1): small-batch UP on the GEMV kernel
+
+template <int NB>
+int launch_gemv_up(const void* w, int64_t w_ld, const int32_t* idx, const int32_t* count_dev, int M, const void* x,
+                   int64_t x_ld, int N, int K, const float* bias, int act, void* out, int64_t out_ld, int out_bf16,
+                   cudaStream_t st) {
+  const size_t smem = (size_t)NB * K * 2;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(gemv_up_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+        cudaSuccess)
+      return PS_ERR_CUDA;
+    configured = true;
+  }
+  const int per_sm = smem <= 100 * 1024 ? 2 : 1;
+  return launch_ex(gemv_up_kernel<NB>, dim3(ps_num_sms() * per_sm), dim3(kGvThreads), smem, st, 1,
+                   static_cast<const uint16_t*>(w), w_ld, idx, count_dev, M, static_cast<const uint16_t*>(x), x_ld,
+                   N, K, bias, act, out, out_ld, out_bf16, BM);
+}
+
 extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                               const void* x, int64_t x_ld, const float* bias, const float* residual,
                               int64_t residual_ld, int N, int M, int K, int act, int splits, int flags, void* out,
@@ -812,6 +933,18 @@ extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* i
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;
   if (w_height < (idx ? 1 : M)) return PS_ERR_VALUE;
+  if (g_gemv < 0) {
+    const char* e = getenv("PS_GG_GEMV");
+    g_gemv = e ? atoi(e) : 1;
+  }
+  if (g_gemv && N <= 4 && !residual && (size_t)16 * K * 2 <= 200 * 1024 && x_ld % 8 == 0 &&
+      ((uintptr_t)x % 16) == 0 && ((uintptr_t)w_rows % 16) == 0) {
+    cudaStream_t s2 = static_cast<cudaStream_t>(stream);
+    const int ob = out_dtype == PS_DTYPE_BF16;
+    if (N <= 1) return launch_gemv_up<1>(w_rows, K, idx, count_dev, M, x, x_ld, N, K, bias, act, out, out_ld, ob, s2);
+    if (N <= 2) return launch_gemv_up<2>(w_rows, K, idx, count_dev, M, x, x_ld, N, K, bias, act, out, out_ld, ob, s2);
+    return launch_gemv_up<4>(w_rows, K, idx, count_dev, M, x, x_ld, N, K, bias, act, out, out_ld, ob, s2);
+  }
   const int rows_est = splits > 0 ? (splits < M ? splits : M) : M;
   return launch<MODE_UP>(prm, w_height, K, K, (rows_est + BM - 1) / BM, (K + BK - 1) / BK,
                          static_cast<cudaStream_t>(stream));
@@ -851,3 +984,4 @@ extern "C" void ps_debug_gemm_trace(void* buf, int stages, int target_ctas) {
 // A-operand copy engine: 0 = TMA only, 1 = LSU for gathered rows (default),
 // 2 = LSU for every A operand.
 extern "C" void ps_debug_gemm_lsu_mode(int mode) { g_lsu_mode = mode; }
+extern "C" void ps_debug_gemm_gemv(int enable) { g_gemv = enable ? 1 : 0; }

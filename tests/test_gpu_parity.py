@@ -433,3 +433,44 @@ def test_kv_append_and_capacity():
     assert torch.equal(c.keys[1, :, 2], k[1]) and torch.equal(c.values[2, :, 3], v[2])
     with pytest.raises(pb.CapacityError):
         c.append_step(k, v)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4])
+def test_small_batch_gemv_up_matches_tiles_and_torch(N):
+    """N <= 4: the UP projection runs on the gathered GEMV (whole rows per
+    warp); it matches the tcgen05 tile path and an fp32 torch reference, and
+    zeroes the padding positions the DOWN projection may read."""
+    from paper_2505_14884_b200 import _lib, kernels as pk
+
+    gen = torch.Generator(device=DEV).manual_seed(N)
+    d, D = 4096, 16384
+    w1t = (torch.randn(D, d, device=DEV, generator=gen) * 0.02).bfloat16()
+    b1 = torch.randn(D, device=DEV, generator=gen) * 0.02
+    x = torch.randn(N, d, device=DEV, generator=gen).bfloat16()
+    rng = np.random.default_rng(N)
+    sel = np.sort(rng.choice(D, 5000 + N, replace=False))
+    nit = pb.NeuronIndexTensor(0, torch.from_numpy(sel).to(DEV, torch.int32), validate=False)
+    count = sel.size
+    pad = -(-count // 128) * 128
+    outs = []
+    L = _lib.load()
+    for gemv in (1, 0):
+        L.ps_debug_gemm_gemv(gemv)
+        try:
+            out = torch.full((N, 16384 + 128), float("nan"), device=DEV).bfloat16()
+            pk.gather_gemm_into(w1t, nit.buffer, nit.count, x, d, b1, N, D, d, _lib.PS_ACT_RELU, out, out.stride(0),
+                                splits=count)
+            torch.cuda.synchronize()
+            outs.append(out)
+        finally:
+            L.ps_debug_gemm_gemv(1)
+    g, tl = outs
+    assert torch.equal(g[:, count:pad], torch.zeros_like(g[:, count:pad]))
+    it = torch.from_numpy(sel).to(DEV)
+    ref = torch.relu(x.double() @ w1t[it].double().T + b1[it].double())
+    for o in (g, tl):
+        got = o[:, :count].double()
+        assert torch.isfinite(got).all()
+        assert (got - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
+    # the two summation orders differ by at most ~1 bf16 ulp of the output
+    assert (g[:, :count].float() - tl[:, :count].float()).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
