@@ -663,7 +663,15 @@ size_t smem_bytes(int NB, int stages) {
   return 1024 + (size_t)stages * (BM * BK * 2 + NB * BK * 2) + 256 + (size_t)kEpiCols * BM * 4;
 }
 
-int cta_slots(int NB) { return g_target_override > 0 ? g_target_override : ps_num_sms() * ctas_per_sm(NB); }
+int cta_slots(int NB) {
+  static const int env_target = [] {  // tuning hook: PS_GG_TARGET = CTA slots per launch
+    const char* e = getenv("PS_GG_TARGET");
+    return e ? atoi(e) : 0;
+  }();
+  if (g_target_override > 0) return g_target_override;
+  if (env_target > 0) return env_target;
+  return ps_num_sms() * ctas_per_sm(NB);
+}
 
 // cluster size: enough CTAs per tile to fill every CTA slot, >= 2 K blocks each
 int pick_cluster(int NB, int tiles_est, int kbt) {
