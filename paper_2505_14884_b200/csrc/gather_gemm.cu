@@ -799,7 +799,9 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
     const char* e = getenv("PS_GG_PUSH");
     g_push = e ? atoi(e) : 1;
   }
-  prm.push = g_push;
+  // push pays while a tile has <= 2 column chunks; at 4 (B = 256) the per-chunk
+  // "slot free" round trips serialise it (UP 41.7 -> 48.1 us, ncu, B = 256)
+  prm.push = g_push && prm.NB <= 2 * kEpiCols;
   prm.vec_ok = (out_ld % 4 == 0) && ((uintptr_t)out % 16 == 0);
   return PS_OK;
 }
