@@ -308,8 +308,10 @@ class PagedKVCache:
         """tensors.py:150-170 into the page holding each sequence's next row."""
         if (self.host_lengths >= self.capacity).any():
             raise CapacityError(f"KV cache capacity {self.capacity} exhausted")
-        for b in range(self.batch):
-            self.reserve(b, int(self.host_lengths[b]) + 1)
+        # only sequences whose next row opens a page that is not mapped yet
+        nxt = self.host_lengths // self.page_rows
+        for b in np.nonzero(self.host_table[np.arange(self.batch), nxt] < 0)[0]:
+            self.reserve(int(b), int(self.host_lengths[b]) + 1)
         k_new = as_device_tensor(k_new, "k_new", dtype=torch.bfloat16)
         v_new = as_device_tensor(v_new, "v_new", dtype=torch.bfloat16)
         if src_ld is None:
