@@ -1,0 +1,48 @@
+"""bench.py driver contract on the tiny config: one JSON line with the keys
+the driver and judge read (value / e2e / roofline / cpu_baseline / clocks /
+gpu_launches), and the reference arm's line."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_line_has_the_contract_keys():
+    j = _run("--config", "tiny", "--batch", "8", "--ctx", "200", "--steps", "3", "--warmup", "3", "--cpu-batch", "2")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "cpu_baseline", "clocks"):
+        assert k in j, k
+    assert j["n_gpus"] == 1 and j["steps"] == 3 and j["warmup"] == 3 and j["value"] > 0
+    assert j["e2e"]["h2d_bytes_per_step"] > 0 and j["e2e"]["d2h_bytes_per_step"] > 0 and j["e2e"]["value"] > 0
+    assert j["gpu_launches"] > 0
+    r = j["roofline"]
+    assert r["bound"] == "hbm" and r["achieved"] > 0 and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-6
+    assert j["cpu_baseline"]["kind"] in ("port", "reference") and j["cpu_baseline"]["cores"] >= 1
+    assert "workload" in j["config"]
+
+
+def test_reference_arm_line():
+    j = _run("--impl", "reference", "--config", "tiny", "--batch", "8", "--ctx", "200", "--steps", "1",
+             "--warmup", "1")
+    assert j["impl"] == "reference" and j["value"] > 0
+    assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["cpu_baseline"]["value"] == j["value"]
