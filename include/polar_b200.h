@@ -179,6 +179,13 @@ int ps_head_router_topk_append(const void* x, int64_t x_ld, const void* w_t, con
                                void* k_cache, void* v_cache, int32_t* lengths,
                                const void* k_new, const void* v_new, int64_t src_ld,
                                int H_cache, int cap, int d_h, int32_t* err_flag, void* stream);
+/* Same, appending into a paged cache (ps_kv_append_paged layout). */
+int ps_head_router_topk_append_paged(const void* x, int64_t x_ld, const void* w_t, const float* bias,
+                                     int B, int d, int H_kv, int k, float* logits_out, int32_t* sel_out,
+                                     void* k_pool, void* v_pool, int page_rows,
+                                     const int32_t* block_table, int64_t table_ld, int32_t* lengths,
+                                     const void* k_new, const void* v_new, int64_t src_ld,
+                                     int H_cache, int d_h, int32_t* err_flag, void* stream);
 
 /* ======================================================================
  * Gathered GEMM on tcgen05 tensor cores (TMEM accumulators).

@@ -50,6 +50,8 @@ SIGNATURES = {
     "ps_head_router_topk": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_head_router_topk_append": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                         _i64, _i, _i, _i, _vp, _vp]),
+    "ps_head_router_topk_append_paged": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp,
+                                              _i64, _vp, _vp, _vp, _i64, _i, _i, _vp, _vp]),
     "ps_debug_gemm_trace": (None, [_vp, _i, _i]),
     "ps_debug_gemm_lsu_mode": (None, [_i]),
     "ps_debug_gemm_gemv": (None, [_i]),

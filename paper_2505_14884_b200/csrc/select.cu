@@ -922,6 +922,10 @@ struct AppendArgs {
   int64_t src_ld;
   int Hc, cap, d_h;
   int32_t* err;
+  // paged caches (pages, Hc, page_rows, d_h): NULL = contiguous (B, Hc, cap, d_h)
+  const int32_t* table;
+  int64_t table_ld;
+  int page_rows;
 };
 
 template <int R>
@@ -965,10 +969,20 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
         continue;
       }
       const int total = max(0, ha1 - ha0) * vph;
+      // row of (b, head 0) at pos, heads `hs` rows apart (contiguous or paged)
+      size_t rb, hs;
+      if (ap.table) {
+        const int pg = __ldg(ap.table + (size_t)b * ap.table_ld + pos / ap.page_rows);
+        rb = (size_t)pg * ap.Hc * ap.page_rows + pos % ap.page_rows;
+        hs = ap.page_rows;
+      } else {
+        rb = (size_t)b * ap.Hc * ap.cap + pos;
+        hs = ap.cap;
+      }
       for (int e = tid; e < total; e += kHrThreads) {
         const int h = ha0 + e / vph, c = e - (e / vph) * vph;
         const size_t src = (size_t)b * ap.src_ld + (size_t)h * ap.d_h + c * 8;
-        const size_t dst = (((size_t)b * ap.Hc + h) * ap.cap + pos) * ap.d_h + c * 8;
+        const size_t dst = (rb + h * hs) * ap.d_h + c * 8;
         const uint4 kv = __ldg(reinterpret_cast<const uint4*>(ap.kn + src));
         const uint4 vv = __ldg(reinterpret_cast<const uint4*>(ap.vn + src));
         *reinterpret_cast<uint4*>(ap.kc + dst) = kv;
@@ -1197,6 +1211,25 @@ extern "C" int ps_head_router_topk_append(const void* x, int64_t x_ld, const voi
     return PS_ERR_VALUE;
   AppendArgs ap{static_cast<uint16_t*>(k_cache), static_cast<uint16_t*>(v_cache), lengths,
                 static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), src_ld, H_cache, cap, d_h,
-                err_flag};
+                err_flag, nullptr, 0, 0};
+  return head_router_common(x, x_ld, w_t, bias, B, d, H_kv, k, logits_out, sel_out, ap, stream);
+}
+
+extern "C" int ps_head_router_topk_append_paged(const void* x, int64_t x_ld, const void* w_t, const float* bias,
+                                                int B, int d, int H_kv, int k, float* logits_out, int32_t* sel_out,
+                                                void* k_pool, void* v_pool, int page_rows,
+                                                const int32_t* block_table, int64_t table_ld, int32_t* lengths,
+                                                const void* k_new, const void* v_new, int64_t src_ld, int H_cache,
+                                                int d_h, int32_t* err_flag, void* stream) {
+  if (!k_pool || !v_pool || !block_table || !lengths || !k_new || !v_new || H_cache < 1 || page_rows < 1 ||
+      table_ld < 1 || d_h < 8 || d_h % 8 || src_ld < (int64_t)H_cache * d_h || src_ld % 8)
+    return PS_ERR_VALUE;
+  if (((uintptr_t)k_new % 16) || ((uintptr_t)v_new % 16) || ((uintptr_t)k_pool % 16) || ((uintptr_t)v_pool % 16))
+    return PS_ERR_VALUE;
+  const long long cap = (long long)table_ld * page_rows;
+  if (cap >= (1ll << 31)) return PS_ERR_VALUE;
+  AppendArgs ap{static_cast<uint16_t*>(k_pool), static_cast<uint16_t*>(v_pool), lengths,
+                static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), src_ld, H_cache, (int)cap,
+                d_h, err_flag, block_table, table_ld, page_rows};
   return head_router_common(x, x_ld, w_t, bias, B, d, H_kv, k, logits_out, sel_out, ap, stream);
 }

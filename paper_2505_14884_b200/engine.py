@@ -323,7 +323,7 @@ class DecodeEngine:
             n += self._linear_bf16(self.h, lw.w_qkv_t, lw.b_qkv, self.qkv, tag="gg_qkv")
             kq = self.qkv[:, self.d_loc:]
             vq = self.qkv[:, self.d_loc + self.dk_loc:]
-            if not k_h or self.concurrent_router or self.paged:
+            if not k_h or self.concurrent_router:
                 st = _lib.stream_ptr()
                 if self.paged:
                     _lib.check(L.ps_kv_append_paged(_lib.ptr(c.k_pool), _lib.ptr(c.v_pool), c.page_rows,
@@ -337,9 +337,6 @@ class DecodeEngine:
                 n += 1
             if k_h and self.concurrent_router:
                 torch.cuda.current_stream().wait_stream(self.side)
-            elif k_h and self.paged:  # the fused head-router append writes contiguous caches only
-                sel = self._head_select(ell, k_h)
-                n += 1
             elif k_h:
                 # head router + top-k fused with the KV append (one launch)
                 sel = self._head_select(ell, k_h, append=(c, kq, vq, qkv_w))

@@ -77,6 +77,13 @@ class HeadRouter:
         """select_into fused with the step's KV append into ``cache``
         (tensors.py:150-170 semantics; one launch instead of two)."""
         B, d = x2d.shape
+        if hasattr(cache, "block_table"):  # PagedKVCache
+            _lib.call("ps_head_router_topk_append_paged", _lib.ptr(x2d), x2d.stride(0), _lib.ptr(self.w_t),
+                      _lib.ptr(self.b), B, d, self.n_heads, int(k), _lib.ptr(logits_out), _lib.ptr(sel_out),
+                      _lib.ptr(cache.k_pool), _lib.ptr(cache.v_pool), cache.page_rows, _lib.ptr(cache.block_table),
+                      cache.max_pages, _lib.ptr(cache.lengths), _lib.ptr(k_new), _lib.ptr(v_new), int(src_ld),
+                      cache.kv_heads, cache.head_dim, _lib.ptr(cache._err), _lib.stream_ptr())
+            return
         _lib.call("ps_head_router_topk_append", _lib.ptr(x2d), x2d.stride(0), _lib.ptr(self.w_t), _lib.ptr(self.b),
                   B, d, self.n_heads, int(k), _lib.ptr(logits_out), _lib.ptr(sel_out), _lib.ptr(cache.keys),
                   _lib.ptr(cache.values), _lib.ptr(cache.lengths), _lib.ptr(k_new), _lib.ptr(v_new), int(src_ld),

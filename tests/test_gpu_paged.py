@@ -145,3 +145,33 @@ def test_engine_step_paged_equals_contiguous(kv_heads, mode):
         a, b = engs[0].step(tokens).clone(), engs[1].step(tokens).clone()
         assert torch.equal(a, b)
     assert engs[1].caches[1].lengths.cpu().tolist() == [257] * 8
+
+
+def test_head_router_fused_append_into_pages():
+    """ps_head_router_topk_append_paged: same selections as the contiguous
+    fused launch, and the same K/V rows land in the pages."""
+    rng = np.random.default_rng(11)
+    B, H_kv, d_h, d = 6, 8, 128, 512
+    c = pb.KVCache(B, H_kv, 200, d_h, device=DEV)
+    c.fill_random(rng, 60)
+    c.set_lengths([60, 63, 64, 95, 96, 127])  # mid-page, page ends and fresh pages (32-row pages)
+    pc = pb.PagedKVCache.from_contiguous(c, page_rows=32, seed=3)
+    hr = pb.HeadRouter(d, H_kv, seed=2)
+    x = torch.randn(B, d, device=DEV).bfloat16()
+    qkv = torch.randn(B, 3 * H_kv * d_h, device=DEV).bfloat16()
+    kq, vq = qkv[:, H_kv * d_h:], qkv[:, 2 * H_kv * d_h:]
+    sel_a = torch.zeros(B, 3, dtype=torch.int32, device=DEV)
+    sel_b = torch.zeros(B, 3, dtype=torch.int32, device=DEV)
+    for b in range(B):  # the caller maps the page each append lands in (as the engine does)
+        pc.reserve(b, int(pc.host_lengths[b]) + 1)
+    hr.select_append_into(x, 3, sel_a, c, kq, vq, qkv.stride(0))
+    hr.select_append_into(x, 3, sel_b, pc, kq, vq, qkv.stride(0))
+    c.host_lengths += 1
+    pc.host_lengths += 1
+    torch.cuda.synchronize()
+    assert torch.equal(sel_a, sel_b)
+    assert pc.lengths.cpu().tolist() == c.lengths.cpu().tolist() == [61, 64, 65, 96, 97, 128]
+    for b in range(B):
+        for h in range(H_kv):
+            assert torch.equal(pc.keys_for(b, h), c.keys_for(b, h))
+            assert torch.equal(pc.values_for(b, h), c.values_for(b, h))
