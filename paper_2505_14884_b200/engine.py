@@ -88,7 +88,7 @@ class DecodeEngine:
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
                  caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
-                 concurrent_router: bool = False, kv_page_rows: int = 0):
+                 concurrent_router: bool = False, kv_page_rows: int = 0, kv_reserve: str = "full"):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
@@ -145,6 +145,10 @@ class DecodeEngine:
         # kv_page_rows > 0: paged caches (block table per sequence, pages
         # reserved for the whole capacity in a scattered order)
         self.kv_page_rows = int(kv_page_rows)
+        # "full": every page of the capacity mapped up front; "on_demand": a
+        # page is mapped (host allocator + one table-row copy) just before the
+        # step whose append enters it -- pool memory follows the actual lengths
+        self.kv_reserve = check_choice(kv_reserve, ("full", "on_demand"), "kv_reserve")
         if self.kv_page_rows and tp is not None:
             raise ValueError("paged KV caches are not wired into tensor parallelism")
 
@@ -152,7 +156,8 @@ class DecodeEngine:
             if self.kv_page_rows:
                 pc = PagedKVCache(batch, self.Hkv_loc, capacity, d_h, page_rows=self.kv_page_rows, device=dev,
                                   seed=1000 + i)
-                pc.reserve_all()
+                if self.kv_reserve == "full":
+                    pc.reserve_all()
                 return pc
             return KVCache(batch, self.Hkv_loc, capacity, d_h, device=dev)
 
@@ -459,6 +464,8 @@ class DecodeEngine:
         """engine.py:314-392: advance every sequence by one token; returns the
         (B, vocab) f32 logits (device).  Uses the captured graph if any."""
         self._check_capacity()
+        if self.paged and self.kv_reserve == "on_demand":
+            self._map_next_pages()
         if tokens is not None:
             tk = torch.as_tensor(np.asarray(tokens) if not isinstance(tokens, torch.Tensor) else tokens)
             if tuple(tk.shape) != (self.B,):
@@ -475,9 +482,24 @@ class DecodeEngine:
         self._advance()
         return self.logits
 
+    def _map_next_pages(self) -> None:
+        """Map the page this step's append enters, for every storage buffer
+        (aliased layers share their base cache's table)."""
+        seen = set()
+        for c in self.caches:
+            key = id(c.block_table)
+            if key in seen:
+                continue
+            seen.add(key)
+            nxt = c.host_lengths // c.page_rows
+            for b in np.nonzero(c.host_table[np.arange(c.batch), nxt] < 0)[0]:
+                c.reserve(int(b), int(c.host_lengths[b]) + 1)
+
     def capture(self, warmup: int = 1) -> None:
         """Capture one step into a CUDA graph (workspaces sized by a warm-up
         step first; the warm-up's KV writes are undone via the lengths)."""
+        if self.paged and self.kv_reserve == "on_demand":
+            self._map_next_pages()  # the warm-up step appends too
         saved = [c.host_lengths.copy() for c in self.caches]
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())

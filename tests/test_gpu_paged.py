@@ -128,8 +128,8 @@ def test_engine_step_paged_equals_contiguous(kv_heads, mode):
     hr = [pb.HeadRouter(256, kv_heads, seed=40 + e) for e in range(2)]
     mr = [pb.MlpRouter(256, 1024, seed=30 + e) for e in range(2)]
     engs = []
-    for pr in (0, 128):  # head_dim 32: the SHA tile is 128 rows
-        e = DecodeEngine(model, 8, 288, pol, head_routers=hr, mlp_routers=mr, kv_page_rows=pr)
+    for pr, rv in ((0, "full"), (128, "full"), (128, "on_demand")):  # head_dim 32: the SHA tile is 128 rows
+        e = DecodeEngine(model, 8, 288, pol, head_routers=hr, mlp_routers=mr, kv_page_rows=pr, kv_reserve=rv)
         rng = np.random.default_rng(22)
         for c in e.caches:
             c.fill_random(rng, 252)
@@ -137,14 +137,16 @@ def test_engine_step_paged_equals_contiguous(kv_heads, mode):
     assert engs[1].paged and not engs[0].paged
     tokens = np.random.default_rng(1).integers(0, 512, 8)
     for _ in range(2):
-        a, b = engs[0].step(tokens).clone(), engs[1].step(tokens).clone()
-        assert torch.equal(a, b)
-    engs[1].capture()
-    engs[0].capture()
+        outs = [e.step(tokens).clone() for e in engs]
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    for e in engs:
+        e.capture()
+    assert (engs[2].caches[1].host_table >= 0).sum() == 2 * 8  # on demand: only pages 0-1 so far
     for _ in range(3):  # crosses the 256-row page boundary (252 + 5 steps)
-        a, b = engs[0].step(tokens).clone(), engs[1].step(tokens).clone()
-        assert torch.equal(a, b)
+        outs = [e.step(tokens).clone() for e in engs]
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     assert engs[1].caches[1].lengths.cpu().tolist() == [257] * 8
+    assert (engs[2].caches[1].host_table >= 0).sum() == 3 * 8  # page 2 mapped when the appends entered it
 
 
 def test_head_router_fused_append_into_pages():
