@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
     ap.add_argument("--kv-page-rows", type=int, default=0,
                     help="paged KV caches with this many rows per page (0 = contiguous)")
+    ap.add_argument("--kv-reserve", default="full", choices=["full", "on_demand"],
+                    help="paged KV: map every page up front, or each page as the appends enter it")
     ap.add_argument("--concurrent-head-router", action="store_true",
                     help="head router as a concurrent graph branch instead of fused with the KV append")
     return ap.parse_args()
@@ -332,7 +334,7 @@ def run_ours(args):
                            mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
     eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring,
                        router_backend=args.router_backend, concurrent_router=args.concurrent_head_router, tp=tp,
-                       kv_page_rows=args.kv_page_rows)
+                       kv_page_rows=args.kv_page_rows, kv_reserve=args.kv_reserve)
     eng.fill_random(ctx, seed=99 + rank)
     dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches, tp=tp)
     tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()

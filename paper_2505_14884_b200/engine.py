@@ -485,6 +485,9 @@ class DecodeEngine:
     def _map_next_pages(self) -> None:
         """Map the page this step's append enters, for every storage buffer
         (aliased layers share their base cache's table)."""
+        c0 = self.caches[0]
+        if not (c0.host_lengths % c0.page_rows == 0).any():
+            return  # no append opens a page this step (every layer advances in lock step)
         seen = set()
         for c in self.caches:
             key = id(c.block_table)
