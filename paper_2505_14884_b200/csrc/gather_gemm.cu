@@ -806,6 +806,9 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
   return PS_OK;
 }
 
+namespace ps {
+namespace {
+
 // ---------------------------------------------------------------------------
 // Small-batch UP projection as a gathered GEMV on CUDA cores (N <= 4; at 8
 // and 16 rows the per-element x unpacking makes it FMA-bound and the tcgen05
@@ -926,6 +929,9 @@ int launch_gemv_up(const void* w, int64_t w_ld, const int32_t* idx, const int32_
                    static_cast<const uint16_t*>(w), w_ld, idx, count_dev, M, static_cast<const uint16_t*>(x), x_ld,
                    N, K, bias, act, out, out_ld, out_bf16, BM);
 }
+
+}  // namespace
+}  // namespace ps
 
 extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                               const void* x, int64_t x_ld, const float* bias, const float* residual,
