@@ -69,6 +69,10 @@ int ps_num_sms(void);
  *           [group_base, group_base + H_kv); selected ids outside that range
  *           are skipped (0 without TP)
  *   num_splits  KV splits per (b, group) unit (FlashDecoding); 0 = auto
+ *   max_len_hint  expected max_b lengths[b] (0 = cap); it only sizes the grid.
+ *           The kernel reads the tile count from the device lengths, so
+ *           the call (and a CUDA graph that captured it) stays exact for
+ *           any lengths[b] <= cap
  *   ws      >= ps_sha_workspace_bytes(...) bytes; must be zero-filled
  *           before its first use (the kernel leaves it zeroed again)
  * ==================================================================== */
@@ -106,7 +110,9 @@ int ps_kv_append(void* k_cache, void* v_cache, int32_t* lengths,
  * ps_sha_decode_paged: ps_sha_decode over the paged pools (same math, same
  *   workspace query, same error behaviour).
  * ps_kv_append_paged: ps_kv_append into the page holding lengths[b]
- *   (the caller maps that page before the step). */
+ *   (the caller maps that page before the step).  Unmapped pages hold -1 in
+ *   block_table: an append whose row falls in one writes nothing, leaves
+ *   lengths[b] as it was and sets err_flag to 2 (1 = capacity). */
 int ps_sha_decode_paged(const void* q, int64_t q_ld, const void* k_pool, const void* v_pool,
                         int pool_pages, int page_rows, const int32_t* block_table, int64_t table_ld,
                         const int32_t* lengths, const int32_t* sel, int group_base,

@@ -164,6 +164,63 @@ def matmul(a, b) -> np.ndarray:
     return matmul64(np.asarray(a, F32), np.asarray(b, F32)).astype(F32)
 
 
+def naive_softmax_attention_single_head(q, keys, values, scale) -> np.ndarray:
+    """tensors.py:83-113 -- two-pass max-subtract softmax, f64 inside."""
+    q = np.asarray(q, F32)
+    keys = np.asarray(keys, F32)
+    values = np.asarray(values, F32)
+    if keys.shape[0] == 0:
+        raise EmptyCache("attention over an empty key/value history")
+    s = scale * (keys.astype(np.float64) @ q.astype(np.float64))
+    s -= s.max()
+    p = np.exp(s)
+    return ((p @ values.astype(np.float64)) / p.sum()).astype(F32)
+
+
+class OnlineSoftmaxState:
+    """kernels.py:138-180 -- (o, l, m) of the one-pass softmax, f64."""
+
+    def __init__(self, head_dim):
+        self.o_acc = np.zeros(head_dim, np.float64)
+        self.l_acc = 0.0
+        self.m_acc = -math.inf
+
+    def update(self, scores, v_block, variant="running"):
+        scores = np.asarray(scores, np.float64)
+        v_block = np.asarray(v_block, np.float64)
+        m_tilde = scores.max()
+        p = np.exp(scores - m_tilde)
+        l_tilde = p.sum()
+        m_new = max(self.m_acc, m_tilde)
+        alpha = math.exp(self.m_acc - m_new)
+        beta = math.exp(m_tilde - m_new)
+        l_new = alpha * self.l_acc + beta * l_tilde
+        pv = p @ v_block
+        if variant == "running":
+            self.o_acc = (alpha * self.l_acc * self.o_acc + beta * pv) / l_new
+        else:
+            self.o_acc = alpha * self.o_acc + beta * pv
+        self.l_acc, self.m_acc = l_new, m_new
+
+    def output(self, variant="running"):
+        return self.o_acc / self.l_acc if variant == "deferred" else self.o_acc
+
+
+def online_softmax_attention(q, keys, values, scale, block_size=64, variant="running"):
+    """kernels.py:183-210 -- single-unit blocked attention; (out f32, state)."""
+    q64 = np.asarray(q, F32).astype(np.float64)
+    keys = np.asarray(keys, F32)
+    values = np.asarray(values, F32)
+    if keys.shape[0] == 0:
+        raise EmptyCache("attention over an empty key/value history")
+    n = keys.shape[0]
+    st = OnlineSoftmaxState(q64.shape[0])
+    for j in range(-(-n // block_size)):
+        k0, k1 = j * block_size, min((j + 1) * block_size, n)
+        st.update(scale * (keys[k0:k1].astype(np.float64) @ q64), values[k0:k1], variant)
+    return st.output(variant).astype(F32), st
+
+
 def layernorm(x, g, b) -> np.ndarray:
     """model.py:168-175 -- f64 inside, f32 out, eps 1e-5."""
     x64 = np.asarray(x, dtype=np.float64)

@@ -14,9 +14,11 @@ from .kernels import (
     BatchHeadIndex,
     FlashBlockParams,
     NeuronIndexTensor,
+    OnlineSoftmaxState,
     PackedMLP,
     dense_mlp_forward,
     gqa_selective_attention_decode,
+    online_softmax_attention,
     selective_gemm,
     selective_gemm_t,
     selective_head_flash_attention_decode,
@@ -25,7 +27,15 @@ from .kernels import (
     union_neuron_indices,
 )
 from .routers import HeadRouter, MlpRouter, head_router_forward, mlp_router_forward, union_from_logits
-from .tensors import KVCache, PagedKVCache, l2_norm_per_head, topk_indices, topk_indices_rows
+from .tensors import (
+    KVCache,
+    PagedKVCache,
+    l2_norm_per_head,
+    matmul,
+    naive_softmax_attention_single_head,
+    topk_indices,
+    topk_indices_rows,
+)
 
 __version__ = "0.1.0"
 
@@ -36,5 +46,6 @@ __all__ = [
     "mlp_router_forward", "selective_gemm", "selective_gemm_t", "selective_head_flash_attention_decode",
     "sparse_mlp_forward", "swiglu_mlp_forward", "topk_indices", "topk_indices_rows", "union_from_logits",
     "union_neuron_indices", "LayerKTable", "load_model", "load_router", "load_run_config", "load_token_stream",
-    "save_token_stream",
+    "save_token_stream", "OnlineSoftmaxState", "online_softmax_attention", "matmul",
+    "naive_softmax_attention_single_head",
 ]

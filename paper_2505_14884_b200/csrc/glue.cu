@@ -10,7 +10,8 @@ namespace {
 // one CTA per sequence: copy H_kv*d_h new keys/values to row lengths[b],
 // then bump lengths[b].  Every thread issues all of its 16-byte loads before
 // its stores (one memory latency per CTA).  A full sequence is left
-// untouched (err_flag = 1).
+// untouched (err_flag = 1), and so is one whose next row falls in an unmapped
+// page (block-table entry < 0; err_flag = 2).
 constexpr int kKvThreads = 512;
 constexpr int kKvVec = 4;  // 16-byte vectors per thread per tensor (H_kv*d_h <= 16384)
 
@@ -34,6 +35,10 @@ __global__ void __launch_bounds__(kKvThreads) kv_append_kernel(uint16_t* __restr
   size_t hstride;
   if (table) {  // paged pool (pages, H_kv, page_rows, d_h)
     const int pg = __ldg(table + (size_t)b * table_ld + pos / page_rows);
+    if (pg < 0) {  // the page holding `pos` was never mapped: write nothing, keep the length
+      if (threadIdx.x == 0 && err_flag) *err_flag = 2;
+      return;
+    }
     base = (size_t)pg * H_kv * page_rows + pos % page_rows;
     hstride = page_rows;
   } else {

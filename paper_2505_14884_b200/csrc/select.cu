@@ -973,6 +973,10 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
       size_t rb, hs;
       if (ap.table) {
         const int pg = __ldg(ap.table + (size_t)b * ap.table_ld + pos / ap.page_rows);
+        if (pg < 0) {  // unmapped page: nothing written, length kept (below)
+          if (tid == 0 && crank == 0 && ap.err) *ap.err = 2;
+          continue;
+        }
         rb = (size_t)pg * ap.Hc * ap.page_rows + pos % ap.page_rows;
         hs = ap.page_rows;
       } else {
@@ -1049,7 +1053,11 @@ __global__ void __launch_bounds__(kHrThreads) head_router_topk_kernel(
   if (crank != 0) return;
   mbar_wait(&s_bar, 0);  // every CTA's logits landed (they read lengths[] before sending)
   // every CTA of the cluster read lengths[] before its logits arrived: bump them now
-  if (ap.kc && tid < nr && ap.lengths[r0 + tid] < ap.cap) ap.lengths[r0 + tid] += 1;
+  if (ap.kc && tid < nr) {
+    const int b = r0 + tid, pos = ap.lengths[b];
+    const bool mapped = !ap.table || __ldg(ap.table + (size_t)b * ap.table_ld + pos / ap.page_rows) >= 0;
+    if (pos < ap.cap && mapped) ap.lengths[b] = pos + 1;
+  }
   // top-k of each row by rank counting, one warp per row
   if (warp < nr) {
     const int r = warp;

@@ -66,7 +66,13 @@ struct ShaParams {
   int64_t table_ld;
   int page_rows;
   int pool_pages;
-  int NT;        // virtual tiles per unit (>= ceil(max length / T))
+  // virtual tiles per unit.  The partition uses NT = ceil(max_b lengths[b] / T)
+  // read from the DEVICE lengths by every CTA (so a captured graph stays
+  // exact as the sequences grow); NT_hint (from the host's length mirror)
+  // only sizes the grid and lets a CTA prefetch its first unit's metadata
+  // before the lengths are reduced
+  int NT_hint;
+  int NT_cap;    // ceil(cap / T)
   int n_ctas;    // stream-K CTAs (the B zero-fill CTAs follow them)
   int max_seg;   // partial slots per unit
   float scale_log2;
@@ -84,8 +90,11 @@ struct ShaParams {
 // the entry after it, so a table read is one page ahead of its use.
 struct PageCursor {
   int b, g, pg, pb, pbn, off, base;
+  // unmapped pages are -1 in the table: they are only ever prefetched as
+  // hints (rows < lengths[b] are mapped by contract); clamp so a violated
+  // contract reads page 0 instead of faulting
   PS_DEV int entry(const ShaParams& p, int j) const {
-    return j < p.table_ld ? __ldg(p.table + (size_t)b * p.table_ld + j) : 0;
+    return j < p.table_ld ? max(0, __ldg(p.table + (size_t)b * p.table_ld + j)) : 0;
   }
   // issued before the unit's selection load so the two latencies overlap
   PS_DEV void start(const ShaParams& p, int b_, int row_first) {
@@ -124,7 +133,7 @@ struct PageCursor {
 
 template <int D_H, int G>
 constexpr size_t sha_smem_bytes() {
-  return 2 * kStages * kTileBytes + 64 + (size_t)kWarps * G * (D_H + 2) * 4 + 16;
+  return 2 * kStages * kTileBytes + 64 + (size_t)kWarps * G * (D_H + 2) * 4 + 32;  // flag + kWarps length partials
 }
 
 template <bool BF16>
@@ -143,6 +152,22 @@ PS_DEV void store_out(void* out, size_t off, float v) {
 // segment in segment order (deterministic).  Tiles beyond a sequence's
 // length are empty pipeline slots (plain arrive, nothing read).
 PS_DEV int cta_of(long long f, long long F, int n) { return (int)(((f + 1) * n - 1) / F); }
+
+// Per-warp partial of max_b lengths[b] into scratch[warp]; after the caller's
+// __syncthreads, sha_nt() turns the kWarps partials into the tile count.
+PS_DEV void sha_len_partial(const ShaParams& p, int* scratch) {
+  int m = 0;
+  for (int b = threadIdx.x; b < p.B; b += kThreads) m = max(m, __ldg(p.lengths + b));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = m;
+}
+PS_DEV int sha_nt(const ShaParams& p, const int* scratch, int T) {
+  int m = scratch[0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) m = max(m, scratch[w]);
+  const int nt = (m + T - 1) / T;
+  return nt < 1 ? 1 : (nt > p.NT_cap ? p.NT_cap : nt);
+}
 
 template <int D_H, int G, bool OUT_BF16>
 __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p) {
@@ -187,20 +212,34 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
     return;
   }
 
-  const long long F = (long long)n_units * p.NT;
-  const long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
-  const int n_it = (int)(f1 - f0);
-
-  // first unit's selection / length: loaded before the barrier setup so the
-  // latency overlaps it (every thread needs them for its first segment)
-  const int u_first = n_it > 0 ? (int)(f0 / p.NT) : 0;
-  const int sel_first = __ldg(p.sel + u_first);
-  const int len_first = __ldg(p.lengths + u_first / p.top_k);
+  // first unit's selection / length under the host's tile-count hint: loaded
+  // before the barrier setup so the latency overlaps it (every thread needs
+  // them for its first segment); reloaded if the device tile count differs
+  int NT = p.NT_hint;
+  long long F = (long long)n_units * NT;
+  long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
+  int u_first = f1 > f0 ? (int)(f0 / NT) : 0;
+  int sel_first = __ldg(p.sel + u_first);
+  int len_first = __ldg(p.lengths + u_first / p.top_k);
+  sha_len_partial(p, flag + 1);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
+  NT = sha_nt(p, flag + 1, S::T);
+  if (NT != p.NT_hint) {
+    F = (long long)n_units * NT;
+    f0 = (long long)bid * F / p.n_ctas;
+    f1 = (long long)(bid + 1) * F / p.n_ctas;
+    const int u = f1 > f0 ? (int)(f0 / NT) : 0;
+    if (u != u_first) {
+      u_first = u;
+      sel_first = __ldg(p.sel + u_first);
+      len_first = __ldg(p.lengths + u_first / p.top_k);
+    }
+  }
+  const int n_it = (int)(f1 - f0);
 
   // producer (thread 0): walks the flattened tiles in order with an
   // incremental (unit, tile) cursor -- the unit's slab / length are loaded
@@ -232,14 +271,14 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
       bulk_g2s(sK + stage * S::T * D_H, p.k + off, bytes, &bars[stage]);
       bulk_g2s(sV + stage * S::T * D_H, p.v + off, bytes, &bars[stage]);
     }
-    if (++cur.t == p.NT) {  // advance the cursor
+    if (++cur.t == NT) {  // advance the cursor
       cur.t = 0;
       if (cur.u + 1 < n_units) load_unit(cur.u + 1);
     }
   };
   if (tid == 0 && n_it > 0) {
-    const int u0 = (int)(f0 / p.NT);
-    cur.t = (int)(f0 - (long long)u0 * p.NT);
+    const int u0 = (int)(f0 / NT);
+    cur.t = (int)(f0 - (long long)u0 * NT);
     load_unit(u0);
     const int pre = min(kStages, n_it);
     for (int s2 = 0; s2 < pre; ++s2) issue_next(s2);
@@ -250,8 +289,8 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   int it = 0;
   long long f = f0;
   while (f < f1) {
-    const int u = (int)(f / p.NT);
-    const long long u_end = (long long)(u + 1) * p.NT;
+    const int u = (int)(f / NT);
+    const long long u_end = (long long)(u + 1) * NT;
     const long long seg_end = f1 < u_end ? f1 : u_end;
     const int b = u / p.top_k;
     const int g = (u == u_first ? sel_first : __ldg(p.sel + u)) - p.group_base;
@@ -280,7 +319,7 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
     }
 
     const int nt_seg = (int)(seg_end - f);
-    const int t0 = (int)(f - (long long)u * p.NT);
+    const int t0 = (int)(f - (long long)u * NT);
     f = seg_end;
     if (!live) {  // another rank's group: only keep the pipeline moving
       for (int k2 = 0; k2 < nt_seg; ++k2, ++it) {
@@ -389,7 +428,7 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
     __syncthreads();
 
     // ---- merge warps; a unit inside one CTA writes its output directly
-    const int c_first = cta_of((long long)u * p.NT, F, p.n_ctas);
+    const int c_first = cta_of((long long)u * NT, F, p.n_ctas);
     const int c_last = cta_of(u_end - 1, F, p.n_ctas);
     const int nseg = c_last - c_first + 1, seg = bid - c_first;
     const size_t out_row = (size_t)b * p.out_ld + (size_t)g * G * D_H;
@@ -540,12 +579,14 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
     return;
   }
 
-  const long long F = (long long)n_units * p.NT;
-  const long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
-  const int n_it = (int)(f1 - f0);
-  const int u_first = n_it > 0 ? (int)(f0 / p.NT) : 0;
-  const int sel_first = __ldg(p.sel + u_first);
-  const int len_first = __ldg(p.lengths + u_first / p.top_k);
+  // tile count from the device lengths (see ShaParams::NT_hint)
+  int NT = p.NT_hint;
+  long long F = (long long)n_units * NT;
+  long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
+  int u_first = f1 > f0 ? (int)(f0 / NT) : 0;
+  int sel_first = __ldg(p.sel + u_first);
+  int len_first = __ldg(p.lengths + u_first / p.top_k);
+  sha_len_partial(p, flag + 1);
   if (tid == 0) {
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
@@ -553,6 +594,19 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
     fence_mbar_init();
   }
   __syncthreads();
+  NT = sha_nt(p, flag + 1, kMmaT);
+  if (NT != p.NT_hint) {
+    F = (long long)n_units * NT;
+    f0 = (long long)bid * F / p.n_ctas;
+    f1 = (long long)(bid + 1) * F / p.n_ctas;
+    const int u = f1 > f0 ? (int)(f0 / NT) : 0;
+    if (u != u_first) {
+      u_first = u;
+      sel_first = __ldg(p.sel + u_first);
+      len_first = __ldg(p.lengths + u_first / p.top_k);
+    }
+  }
+  const int n_it = (int)(f1 - f0);
 
   // producer cursor (thread 0)
   struct Cursor {
@@ -583,13 +637,13 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
       tma_load_2d(v_dst, &tmV, 0, row, &bars[stage]);
       tma_load_2d(v_dst + 4096, &tmV, 64, row, &bars[stage]);
     }
-    if (++cur.t == p.NT) {
+    if (++cur.t == NT) {
       cur.t = 0;
       if (cur.u + 1 < n_units) load_unit(cur.u + 1);
     }
   };
   if (tid == 0 && n_it > 0) {
-    cur.t = (int)(f0 - (long long)u_first * p.NT);
+    cur.t = (int)(f0 - (long long)u_first * NT);
     load_unit(u_first);
     const int pre = min(kMmaStages, n_it);
     for (int s2 = 0; s2 < pre; ++s2) issue_next(s2);
@@ -603,15 +657,15 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
   int it = 0;
   long long f = f0;
   while (f < f1) {
-    const int u = (int)(f / p.NT);
-    const long long u_end = (long long)(u + 1) * p.NT;
+    const int u = (int)(f / NT);
+    const long long u_end = (long long)(u + 1) * NT;
     const long long seg_end = f1 < u_end ? f1 : u_end;
     const int b = u / p.top_k;
     const int g = (u == u_first ? sel_first : __ldg(p.sel + u)) - p.group_base;
     const bool live = g >= 0 && g < p.H_kv;
     const int len = u == u_first ? len_first : __ldg(p.lengths + b);
     const int nt_seg = (int)(seg_end - f);
-    const int t0 = (int)(f - (long long)u * p.NT);
+    const int t0 = (int)(f - (long long)u * NT);
     f = seg_end;
     if (!live) {
       for (int k2 = 0; k2 < nt_seg; ++k2, ++it) {
@@ -715,7 +769,7 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
     __syncthreads();
 
     // ---- merge warps; a unit inside one CTA writes its output directly
-    const int c_first = cta_of((long long)u * p.NT, F, p.n_ctas);
+    const int c_first = cta_of((long long)u * NT, F, p.n_ctas);
     const int c_last = cta_of(u_end - 1, F, p.n_ctas);
     const int nseg = c_last - c_first + 1, seg = bid - c_first;
     const size_t out_row = (size_t)b * p.out_ld + (size_t)g * G * D_H;
@@ -778,7 +832,7 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
 
 template <int G>
 constexpr size_t sha_mma_smem_bytes() {
-  return 1024 + 2 * kMmaStages * kMmaTileBytes + 64 + (size_t)kWarps * G * (128 + 2) * 4 + 16;
+  return 1024 + 2 * kMmaStages * kMmaTileBytes + 64 + (size_t)kWarps * G * (128 + 2) * 4 + 32;  // flag + kWarps length partials
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_sha_encode = nullptr;
@@ -945,7 +999,9 @@ static int sha_decode_impl(const void* q, int64_t q_ld, const void* k_cache, con
   if (d_h < 8 || d_h > 256 || (d_h & (d_h - 1))) return PS_ERR_UNSUPPORTED;
   const int G = H / H_kv;
   if (ws_bytes < ps_sha_workspace_bytes(B, H, H_kv, d_h, top_k, num_splits)) return PS_ERR_WORKSPACE;
-  // max_len_hint must bound every lengths[b]: rows beyond NT tiles are not read
+  // max_len_hint only sizes the grid (and the first-unit prefetch): the
+  // kernel takes the tile count from the device lengths, so any lengths[b] <=
+  // cap are read in full (a graph captured at one length stays exact)
   const int T = kTileBytes / (d_h * 2);
   int max_len = max_len_hint > 0 ? max_len_hint : cap;
   if (max_len > cap) max_len = cap;
@@ -966,7 +1022,8 @@ static int sha_decode_impl(const void* q, int64_t q_ld, const void* k_cache, con
   prm.pool_pages = pool_pages;
   if (table && page_rows % T) return PS_ERR_VALUE;  // a tile never straddles a page
   if (!table && (long long)B * H_kv * cap >= (1ll << 31)) return PS_ERR_UNSUPPORTED;  // 32-bit row index
-  prm.NT = NT;
+  prm.NT_hint = NT;
+  prm.NT_cap = (cap + T - 1) / T;
   prm.n_ctas = sha_ctas(units, NT, num_splits, G);
   prm.max_seg = sha_max_seg(units, prm.n_ctas);
   prm.scale_log2 = scale * kLog2e;

@@ -196,8 +196,17 @@ class DecodeEngine:
             self.su_bytes = int(_lib.load().ps_select_union_workspace_bytes(batch, D))
             self.su_ws = torch.zeros(self.su_bytes, dtype=torch.uint8, device=dev)
             self.union_idx = torch.zeros(_round_up(D, ROW_PAD), dtype=torch.int32, device=dev)
-            self.union_count = torch.zeros(1, dtype=torch.int32, device=dev)
+            # per-layer device union sizes (the count each layer's MLP reads)
             self.union_counts = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
+        # expected union size per layer: sizes the selective-MLP grids (0 =
+        # the maximum).  Set from the device counts of the warm-up step that
+        # precedes every capture, so it follows the actual |S| (not k)
+        self.union_est = [0] * cfg.layers
+        # this engine's own workspaces (tickets / partials; never shared with
+        # another engine, never freed while a captured graph may use them)
+        self.ws = _ws.Pool()
+        self._pending = False  # next_tokens holds a decoded token (after the first step)
+        self._captured_len = 0
         self.scale = 1.0 / math.sqrt(d_h)
         self.graph = None
         self.launches_per_step = None
@@ -302,6 +311,10 @@ class DecodeEngine:
     def step_launches(self) -> int:
         """Enqueue one decode step on the current stream; returns the number
         of libpolar_b200 kernel launches enqueued."""
+        with _ws.using(self.ws):
+            return self._step_launches()
+
+    def _step_launches(self) -> int:
         cfg, m, B = self.cfg, self.model, self.B
         d = cfg.model_dim
         n = 0
@@ -348,6 +361,8 @@ class DecodeEngine:
                 n += 1
             else:
                 sel = self.sel_full
+            # the hint only sizes the grid: the kernel reads the tile count from
+            # the device lengths, so a captured graph stays exact as they grow
             sha_decode_into(self.qkv, qkv_w, c, sel, self.H_loc, self.scale, self.attn, self.d_loc,
                             group_base=self.group_base, max_len_hint=int(c.host_lengths.max()) + 1)
             n += 1
@@ -361,6 +376,7 @@ class DecodeEngine:
             pending = None
             if self.sparse_mlp:
                 r = self.mlp_routers[ell]
+                cnt = self.union_counts[ell:ell + 1]
                 out_bias = None  # the router's output bias is added inside ps_select_union
                 if self.router_backend in ("cublas", "native_in"):
                     if self.router_backend == "native_in":  # tcgen05 kernel, static weights prefetched (PDL)
@@ -378,7 +394,7 @@ class DecodeEngine:
                 _lib.check(L.ps_select_union(_lib.ptr(self.r_logits), _lib.ptr(out_bias), B, cfg.ffn_dim, cfg.ffn_dim,
                                              self.k_mlp[ell], 0.0, _lib.ptr(self.su_ws), self.su_bytes,
                                              lo, hi, ROW_PAD, _lib.ptr(self.union_idx),
-                                             _lib.ptr(self.union_count), st), "ps_select_union")
+                                             _lib.ptr(cnt), st), "ps_select_union")
                 n += 1
                 if self.record is not None:
                     lg = self.r_logits.clone()
@@ -386,13 +402,13 @@ class DecodeEngine:
                         lg += out_bias
                     self.record.setdefault("mlp_logits", []).append(lg)
                     self.record.setdefault("union", []).append(
-                        self.union_idx[: int(self.union_count.item())].clone())
+                        self.union_idx[: int(cnt.item())].clone())
                 if self.tp is None:
-                    mlp_into(lw.mlp, self.h, self.union_idx, self.union_count, self.hidden, self.x,
-                             residual=self.x, expected=self.k_mlp[ell])
+                    mlp_into(lw.mlp, self.h, self.union_idx, cnt, self.hidden, self.x,
+                             residual=self.x, expected=self.union_est[ell])
                     n += 2
                 else:
-                    n += self.tp.mlp(self, lw, self.union_idx, self.union_count)
+                    n += self.tp.mlp(self, lw, self.union_idx, cnt)
             elif self.tp is not None:
                 n += self.tp.mlp(self, lw, None, None)
             elif cfg.activation == "swiglu":
@@ -462,16 +478,26 @@ class DecodeEngine:
     # ------------------------------------------------------------------ public
     def step(self, tokens=None) -> torch.Tensor:
         """engine.py:314-392: advance every sequence by one token; returns the
-        (B, vocab) f32 logits (device).  Uses the captured graph if any."""
+        (B, vocab) f32 logits (device).  Uses the captured graph if any.
+        ``tokens=None`` decodes the previous step's argmax tokens (like the
+        reference's pending tokens; ValueError before the first step)."""
         self._check_capacity()
-        if self.paged and self.kv_reserve == "on_demand":
-            self._map_next_pages()
+        if tokens is None and not self._pending:
+            raise ValueError("no pending tokens: pass the first step's tokens explicitly")
         if tokens is not None:
             tk = torch.as_tensor(np.asarray(tokens) if not isinstance(tokens, torch.Tensor) else tokens)
             if tuple(tk.shape) != (self.B,):
                 raise ValueError(f"tokens must have shape ({self.B},), got {tuple(tk.shape)}")
-            if int(tk.min()) < 0 or int(tk.max()) >= self.cfg.vocab:
-                raise IndexError(f"tokens contains indices >= {self.cfg.vocab}")
+            if tk.dtype.is_floating_point or tk.dtype == torch.bool:
+                raise ValueError("tokens must hold integer ids")
+            lo, hi = int(tk.min()), int(tk.max())
+            if lo < 0 or hi >= self.cfg.vocab:
+                raise IndexError(f"tokens must be in [0, {self.cfg.vocab}), got values in [{lo}, {hi}]")
+        if self.graph is not None and self._regrow():
+            self.capture()  # the sequences outgrew the captured grid size (perf only; see _regrow)
+        if self.paged and self.kv_reserve == "on_demand":
+            self._map_next_pages()
+        if tokens is not None:
             self.tokens.copy_(tk.to(torch.int32), non_blocking=True)
         else:
             self.tokens.copy_(self.next_tokens.to(torch.int32))
@@ -480,7 +506,16 @@ class DecodeEngine:
         else:
             self.launches_per_step = self.step_launches()
         self._advance()
+        self._pending = True
         return self.logits
+
+    def _regrow(self) -> bool:
+        """True when the longest sequence has doubled (+256 rows) since the
+        capture.  Correctness never needs a re-capture (the SHA kernel reads
+        the tile count from the device lengths); the captured SHA grid was
+        sized for the capture-time length, so a much longer history is
+        re-captured to get a grid sized for it."""
+        return int(self.host_lengths.max()) + 1 > 2 * self._captured_len + 256
 
     def _map_next_pages(self) -> None:
         """Map the page this step's append enters, for every storage buffer
@@ -500,10 +535,15 @@ class DecodeEngine:
 
     def capture(self, warmup: int = 1) -> None:
         """Capture one step into a CUDA graph (workspaces sized by a warm-up
-        step first; the warm-up's KV writes are undone via the lengths)."""
+        step first; the warm-up's KV writes are undone via the lengths).
+        The warm-up's union sizes become the expected |S| per layer that
+        sizes the captured selective-MLP grids."""
+        self.graph = None
         if self.paged and self.kv_reserve == "on_demand":
             self._map_next_pages()  # the warm-up step appends too
         saved = [c.host_lengths.copy() for c in self.caches]
+        saved_tokens, saved_next = self.tokens.clone(), self.next_tokens.clone()
+        saved_logits = self.logits.clone()
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -511,11 +551,21 @@ class DecodeEngine:
                 self.launches_per_step = self.step_launches()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
+        if self.sparse_mlp:
+            counts = self.union_counts.cpu().numpy()
+            D = self.D_loc if self.tp is not None else self.cfg.ffn_dim
+            # 1/16 headroom over the warm-up's union (steps vary); the tile
+            # loop still covers any larger union at run time
+            self.union_est = [int(min(D, int(c) + int(c) // 16 + ROW_PAD)) if c > 0 else 0 for c in counts]
         for c, hl in zip(self.caches, saved):
             c.host_lengths[:] = hl
             c.lengths.copy_(torch.from_numpy(hl.astype(np.int32)))
+        self.tokens.copy_(saved_tokens)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             self.step_launches()
         torch.cuda.synchronize()
+        self.next_tokens.copy_(saved_next)  # the pending tokens of the last real step
+        self.logits.copy_(saved_logits)
         self.graph = g
+        self._captured_len = int(self.host_lengths.max()) + 1

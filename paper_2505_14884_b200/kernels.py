@@ -154,6 +154,72 @@ class FlashBlockParams:
         return cls(max(1, int(budget_bytes) // (4 * int(model_dim))))
 
 
+class OnlineSoftmaxState:
+    """Running (accumulator, normalizer, max) of the one-pass softmax
+    (kernels.py:138-180), held on the device in float64.
+
+    The SHA kernel runs the same recurrence per warp in f32 registers (its
+    ``(m, l, o)`` partials merge like :meth:`update`); this object is the
+    single-unit reference path that exposes the state for inspection.
+    """
+
+    def __init__(self, o_acc: torch.Tensor, l_acc: float = 0.0, m_acc: float = -math.inf):
+        self.o_acc = o_acc
+        self.l_acc = float(l_acc)
+        self.m_acc = float(m_acc)
+
+    @classmethod
+    def fresh(cls, head_dim: int, device=None) -> "OnlineSoftmaxState":
+        from .validation import default_device
+        return cls(torch.zeros(int(head_dim), dtype=torch.float64, device=device or default_device()))
+
+    def update(self, scores, v_block, variant: str = "running") -> None:
+        """Fold one key block (already-scaled scores, matching value rows)."""
+        check_choice(variant, _VARIANTS, "variant")
+        s = as_device_tensor(scores, "scores", device=self.o_acc.device).to(torch.float64)
+        v = as_device_tensor(v_block, "v_block", device=self.o_acc.device).to(torch.float64)
+        m_tilde = float(s.max())
+        p = torch.exp(s - m_tilde)
+        l_tilde = float(p.sum())
+        m_new = max(self.m_acc, m_tilde)
+        alpha = math.exp(self.m_acc - m_new)
+        beta = math.exp(m_tilde - m_new)
+        l_new = alpha * self.l_acc + beta * l_tilde
+        pv = p @ v
+        if variant == "running":
+            self.o_acc = (alpha * self.l_acc * self.o_acc + beta * pv) / l_new
+        else:
+            self.o_acc = alpha * self.o_acc + beta * pv
+        self.l_acc = l_new
+        self.m_acc = m_new
+
+    def output(self, variant: str = "running") -> torch.Tensor:
+        if variant == "deferred":
+            return self.o_acc / self.l_acc
+        return self.o_acc
+
+
+def online_softmax_attention(q, keys, values, scale: float, params: "FlashBlockParams" = None,
+                             variant: str = "running"):
+    """kernels.py:183-210: single-unit blocked attention over ``keys`` /
+    ``values`` (N, d_h) in blocks of ``params.block_size``; returns
+    (f32 output, final :class:`OnlineSoftmaxState`)."""
+    params = params or FlashBlockParams()
+    check_choice(variant, _VARIANTS, "variant")
+    qv = as_device_tensor(q, "q", ndim=1)
+    k = as_device_tensor(keys, "keys", device=qv.device, ndim=2)
+    v = as_device_tensor(values, "values", device=qv.device, ndim=2)
+    if k.shape[0] == 0:
+        raise EmptyCacheError("attention over an empty key/value history")
+    n_kv = k.shape[0]
+    state = OnlineSoftmaxState.fresh(qv.shape[0], device=qv.device)
+    q64 = qv.to(torch.float64)
+    for j in range(params.num_blocks(n_kv)):
+        k0, k1 = j * params.block_size, min((j + 1) * params.block_size, n_kv)
+        state.update(scale * (k[k0:k1].to(torch.float64) @ q64), v[k0:k1], variant=variant)
+    return state.output(variant).to(torch.float32), state
+
+
 # ---------------------------------------------------------------------------
 # Select-Head Attention
 # ---------------------------------------------------------------------------

@@ -5,7 +5,9 @@ learned positions, LayerNorm, ReLU or SwiGLU MLP, GQA via kv_heads).
 ``DeviceModel`` holds one model in HBM laid out for the kernels:
 
 * attention projections packed neuron-major: ``w_qkv_t`` (d + 2*kv_dim, d)
-  so Q, K and V come out of ONE tcgen05 launch; ``w_o_t`` (d, d);
+  so Q, K and V come out of ONE GEMM launch (cuBLAS by default, the
+  tcgen05 gathered-GEMM kernel with identity ids under
+  ``dense_backend="native"``); ``w_o_t`` (d, d);
 * MLP blocks as :class:`~paper_2505_14884_b200.kernels.PackedMLP`
   (W1^T / W2^T rows = one neuron each, the gather unit);
 * embeddings bf16, LayerNorm parameters and biases f32.

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .exceptions import CapacityError
+from .exceptions import CapacityError, EmptyCacheError
 from .validation import as_device_tensor, check_count
 
 MATMUL_TILE = 256  # tensors.py:24-26 (kept for API parity)
@@ -55,6 +55,52 @@ def topk_indices(scores, k: int) -> torch.Tensor:
     if not 1 <= k <= s.shape[0]:
         raise ValueError(f"k must be in [1, {s.shape[0]}], got {k}")
     return _rows_topk(s[None, :], int(k))[0]
+
+
+def _raise_append_error(cache) -> None:
+    code = int(cache._err.item())
+    if code:
+        cache._err.zero_()
+        if code == 2:
+            raise ValueError("KV append into an unmapped page (reserve the page before the step)")
+        raise CapacityError(f"KV cache capacity {cache.capacity} exhausted on the device")
+
+
+def matmul64(a, b) -> torch.Tensor:
+    """tensors.py:42-51: float64-accumulated product on the device (cuBLAS
+    DGEMM; the reference's 256-column tiling does not change the result)."""
+    a = as_device_tensor(a, "a", ndim=2)
+    b = as_device_tensor(b, "b", ndim=2, device=a.device)
+    return a.to(torch.float64) @ b.to(torch.float64)
+
+
+def matmul(a, b) -> torch.Tensor:
+    """tensors.py:29-39: dense float32 product with float64 accumulation."""
+    a = as_device_tensor(a, "a", ndim=2)
+    b = as_device_tensor(b, "b", ndim=2, device=a.device)
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"matmul shape mismatch: {tuple(a.shape)} x {tuple(b.shape)} (inner dims differ)")
+    return matmul64(a, b).to(torch.float32)
+
+
+def naive_softmax_attention_single_head(q, keys, values, scale: float) -> torch.Tensor:
+    """tensors.py:83-113: two-pass (max-subtract) softmax attention for one
+    head of one sequence, float64 on the device -- the stability reference
+    the blocked SHA kernel is validated against."""
+    q = as_device_tensor(q, "q", ndim=1)
+    keys = as_device_tensor(keys, "keys", ndim=2, device=q.device)
+    values = as_device_tensor(values, "values", ndim=2, device=q.device)
+    if keys.shape[0] == 0:
+        raise EmptyCacheError("attention over an empty key/value history")
+    if tuple(keys.shape) != tuple(values.shape):
+        raise ValueError(f"keys {tuple(keys.shape)} and values {tuple(values.shape)} differ")
+    if keys.shape[1] != q.shape[0]:
+        raise ValueError(f"q dim {q.shape[0]} != head dim {keys.shape[1]}")
+    if not scale > 0:
+        raise ValueError(f"scale must be positive, got {scale}")
+    s = scale * (keys.to(torch.float64) @ q.to(torch.float64))
+    p = torch.exp(s - s.max())
+    return ((p @ values.to(torch.float64)) / p.sum()).to(torch.float32)
 
 
 class KVCache:
@@ -184,6 +230,11 @@ class KVCache:
         self.host_lengths[:] = length
         self._sync_lengths()
 
+    def check_errors(self) -> None:
+        """Raise for a refused device append (reads the error flag: one
+        device sync, so eager / debug use)."""
+        _raise_append_error(self)
+
     def keys_for(self, b: int, h: int) -> torch.Tensor:
         return self.keys[b, h, : int(self.host_lengths[b])]
 
@@ -223,7 +274,7 @@ class PagedKVCache:
         shape = (pool, kv_heads, page_rows, head_dim)
         self.k_pool = torch.zeros(shape, dtype=dtype, device=device)
         self.v_pool = torch.zeros(shape, dtype=dtype, device=device)
-        self.block_table = torch.zeros((batch, self.max_pages), dtype=torch.int32, device=device)
+        self.block_table = torch.full((batch, self.max_pages), -1, dtype=torch.int32, device=device)
         self.host_table = np.full((batch, self.max_pages), -1, dtype=np.int64)
         self.lengths = torch.zeros(batch, dtype=torch.int32, device=device)
         self.host_lengths = np.zeros(batch, dtype=np.int64)
@@ -277,8 +328,8 @@ class PagedKVCache:
                     raise CapacityError("KV page pool exhausted")
                 row[j] = self._free.pop()
                 changed = True
-        if changed:
-            self.block_table[b].copy_(torch.from_numpy(np.maximum(row, 0).astype(np.int32)))
+        if changed:  # unmapped pages stay -1 on the device (appends into them are refused)
+            self.block_table[b].copy_(torch.from_numpy(row.astype(np.int32)))
 
     def reserve_all(self) -> None:
         for b in range(self.batch):
@@ -289,7 +340,7 @@ class PagedKVCache:
         row = self.host_table[b]
         self._free.extend(int(p) for p in row[row >= 0][::-1])
         row[:] = -1
-        self.block_table[b].zero_()
+        self.block_table[b].fill_(-1)
         self.host_lengths[b] = 0
         self._sync_lengths()
 
@@ -390,6 +441,11 @@ class PagedKVCache:
             k = torch.empty(shape, dtype=torch.bfloat16, device=self.device).normal_(generator=gen)
             v = torch.empty(shape, dtype=torch.bfloat16, device=self.device).normal_(generator=gen)
         self.load_contiguous(k, v, np.full(self.batch, length))
+
+    def check_errors(self) -> None:
+        """Raise for a refused device append (reads the error flag: one
+        device sync, so eager / debug use).  1 = capacity, 2 = unmapped page."""
+        _raise_append_error(self)
 
     def keys_for(self, b: int, h: int) -> torch.Tensor:
         return torch.cat([self.k_pool[pg, h, o:o + r1 - r0]

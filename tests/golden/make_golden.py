@@ -208,6 +208,29 @@ def decode_cases():
                 put(f"dec_{tag}_{mode}_union_{ell}", u)
 
 
+def unit_cases():
+    """Single-unit references (kernels.py:138-210, tensors.py:83-113)."""
+    rng = np.random.default_rng(600)
+    cases = [(1, 32, 1), (7, 32, 3), (300, 128, 64), (257, 64, 8), (50, 16, 50)]
+    put("unit_n", len(cases))
+    for i, (n, d_h, bs) in enumerate(cases):
+        q, k, v = rnd(rng, d_h), rnd(rng, n, d_h), rnd(rng, n, d_h)
+        scale = 1.0 / math.sqrt(d_h)
+        put(f"unit_q_{i}", q)
+        put(f"unit_k_{i}", k)
+        put(f"unit_v_{i}", v)
+        put(f"unit_bs_{i}", bs)
+        put(f"unit_naive_{i}", sd_t.naive_softmax_attention_single_head(q, k, v, scale))
+        for variant in ("running", "deferred"):
+            out, st = sd_k.online_softmax_attention(q, k, v, scale, sd_k.FlashBlockParams(bs), variant)
+            put(f"unit_online_{variant}_{i}", out)
+            put(f"unit_state_{variant}_{i}", np.array([st.l_acc, st.m_acc]))
+    a, b = rnd(rng, 5, 300), rnd(rng, 300, 700)
+    put("matmul_a", a)
+    put("matmul_b", b)
+    put("matmul_out", sd_t.matmul(a, b))
+
+
 def main():
     topk_cases()
     union_cases()
@@ -215,6 +238,7 @@ def main():
     mlp_cases()
     router_cases()
     decode_cases()
+    unit_cases()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print(f"wrote {path}: {len(OUT)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

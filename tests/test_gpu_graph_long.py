@@ -1,0 +1,133 @@
+"""Long CUDA-graph replays against the oracle (VERDICT r1 "What's weak" #1).
+
+A decode step captured at one cache length must keep reading every row
+``[0, lengths[b])`` on every replay, however far the sequences have grown
+since the capture (reference semantics: kernels.py:386-444 reads
+``lengths[b]`` rows on every call).  The SHA kernel takes its tile count
+from the device lengths, so these tests capture once and replay >= 3 SHA
+tiles (32 rows each at d_h = 128) past the capture-time window, comparing
+every replayed step with
+
+* an eager (uncaptured) engine fed the same tokens, and
+* the numpy oracle's ``decode_step`` forced to the eager engine's
+  (bit-exactly checked) selections, run in lock step from identical caches.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import polar_oracle as po
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2505_14884_b200 as pb  # noqa: E402
+from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy  # noqa: E402
+from paper_2505_14884_b200.model import DeviceModel, TransformerConfig  # noqa: E402
+
+L, D_MODEL, FFN, HEADS, VOCAB, MAXSEQ = 2, 512, 1024, 4, 256, 512  # d_h = 128: 32-row SHA tiles
+K_MLP = 256
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def _setup(kv_heads, mode, B, lengths, paged=0):
+    cfg = TransformerConfig(L, D_MODEL, FFN, HEADS, kv_heads, VOCAB, MAXSEQ, "relu")
+    host = po.random_model(L, D_MODEL, FFN, HEADS, kv_heads, VOCAB, MAXSEQ, seed=7)
+    model = DeviceModel.from_host(cfg, host)
+    polar = mode == "polar"
+    policy = SparsityPolicy(mode=mode, mlp_k_table={e: K_MLP for e in range(L)} if polar else None,
+                            head_density=0.5 if polar else 1.0)
+    hr = [pb.HeadRouter(D_MODEL, kv_heads, seed=60 + e) for e in range(L)]
+    mr = [pb.MlpRouter(D_MODEL, FFN, seed=70 + e) for e in range(L)]
+
+    def engine(**kw):
+        eng = DecodeEngine(model, B, MAXSEQ, policy, head_routers=hr, mlp_routers=mr, **kw)
+        rng = np.random.default_rng(3)
+        for c in eng.caches:
+            c.fill_random(rng, int(max(lengths)))
+            c.set_lengths(lengths)
+        return eng
+
+    eager = engine()
+    graph = engine(kv_page_rows=paged, kv_reserve="on_demand") if paged else engine()
+    rng = np.random.default_rng(3)
+    caches = []
+    for _ in range(L):
+        c = po.KVCache(B, kv_heads, MAXSEQ, D_MODEL // HEADS)
+        c.fill_random(rng, int(max(lengths)))
+        c.lengths[:] = lengths
+        caches.append(c)
+    routers = [po.init_mlp_router(D_MODEL, FFN, seed=70 + e) for e in range(L)]
+    return host, eager, graph, caches, routers, policy
+
+
+@pytest.mark.parametrize("kv_heads,mode,paged", [(4, "polar", 0), (4, "dense", 0), (2, "polar", 0),
+                                                 (4, "polar", 64)])
+def test_captured_graph_reads_rows_appended_after_capture(kv_heads, mode, paged):
+    B = 4
+    lengths = np.array([100, 37, 129, 64])
+    host, eager, graph, caches, routers, policy = _setup(kv_heads, mode, B, lengths, paged)
+    graph.capture()  # window at capture: ceil(130 / 32) = 5 tiles = 160 rows
+    steps = 110      # the longest sequence reaches 239 rows (> 2 tiles past the window)
+    tok_rng = np.random.default_rng(11)
+    worst = 0.0
+    for s in range(steps):
+        tokens = tok_rng.integers(0, VOCAB, B)
+        eager.record = {}
+        le = eager.step(tokens).clone()
+        lg = graph.step(tokens).clone()
+        # graph replay == eager step (f32-rounding level: shared GEMM tiles)
+        assert torch.allclose(le, lg, rtol=1e-3, atol=1e-4), f"step {s}: replay diverged from eager"
+        rec = eager.record
+        forced = {"heads": {}, "union": {}}
+        if mode == "polar":
+            forced["heads"][1] = rec["heads"][0].cpu().numpy()
+            for e in range(L):
+                forced["union"][e] = rec["union"][e].cpu().numpy()
+        ref = po.decode_step(host, caches, tokens, mode=mode, head_density=policy.head_density,
+                             k_table=policy.mlp_k_table, head_routers=[None] * L, mlp_routers=routers,
+                             forced=forced)
+        r = _rel(lg.cpu().numpy(), ref)
+        worst = max(worst, r)
+        assert r <= 2e-2, f"step {s}: rel err {r:.3e} vs the oracle"
+    final = lengths + steps
+    assert np.array_equal(graph.host_lengths, final)
+    assert graph.caches[1].lengths.cpu().numpy().tolist() == final.tolist()
+    assert np.array_equal(caches[0].lengths, final)
+
+
+def test_public_sha_reads_full_length_with_stale_hint():
+    """ps_sha_decode with a max_len_hint below the device lengths still reads
+    every row (the hint only sizes the grid)."""
+    from paper_2505_14884_b200.kernels import sha_decode_into
+    B, H, d_h = 3, 4, 128
+    rng = np.random.default_rng(0)
+    cache = pb.KVCache(B, H, 512, d_h)
+    cache.fill_random(rng, 400)
+    cache.set_lengths([400, 250, 333])
+    q = torch.from_numpy(rng.standard_normal((B, H * d_h), dtype=np.float32)).cuda().to(torch.bfloat16)
+    sel = torch.tensor([[0, 2], [1, 3], [0, 3]], dtype=torch.int32, device="cuda")
+    outs = []
+    for hint in (0, 33, 401):
+        out = torch.empty(B, H * d_h, dtype=torch.float32, device="cuda")
+        sha_decode_into(q, H * d_h, cache, sel, H, 1 / np.sqrt(d_h), out, H * d_h, max_len_hint=hint)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[2])
+    assert torch.allclose(outs[0], outs[1], rtol=1e-5, atol=1e-6)
+    ref_cache = po.KVCache(B, H, 512, d_h)
+    ref_cache.keys[:] = cache.keys.float().cpu().numpy()
+    ref_cache.values[:] = cache.values.float().cpu().numpy()
+    ref_cache.lengths[:] = [400, 250, 333]
+    q4 = q.float().cpu().numpy().reshape(B, H, 1, d_h)
+    ref = po.gqa_selective_attention_decode(q4, ref_cache, sel.cpu().numpy().astype(np.int64))
+    got = outs[1].cpu().numpy().reshape(B, H, 1, d_h)
+    assert np.abs(got - ref).max() <= 2e-2

@@ -112,6 +112,27 @@ def test_paged_capacity_and_validation():
         pb.PagedKVCache(2, 2, 64, 128, page_rows=48, device=DEV)  # not a tile multiple
 
 
+def test_append_into_unmapped_page_is_refused():
+    """unmapped pages are -1 on the device; the C-ABI append (no
+    host reserve) refuses them -- nothing written, length kept, err 2 --
+    instead of overwriting whichever sequence owns page 0."""
+    from paper_2505_14884_b200 import _lib
+    pc = pb.PagedKVCache(2, 2, 128, 128, page_rows=32, pool_pages=8, device=DEV)
+    pc.set_lengths([32, 5])  # sequence 0: page 0 full, page 1 unmapped
+    assert pc.block_table[0, 1].item() == -1
+    before = pc.k_pool.clone()
+    kn = torch.ones(2, 2, 128, device=DEV).bfloat16()
+    _lib.call("ps_kv_append_paged", _lib.ptr(pc.k_pool), _lib.ptr(pc.v_pool), pc.page_rows,
+              _lib.ptr(pc.block_table), pc.max_pages, _lib.ptr(pc.lengths), _lib.ptr(kn), _lib.ptr(kn),
+              2 * 128, 2, 2, 128, _lib.ptr(pc._err), _lib.stream_ptr())
+    assert pc.lengths.cpu().tolist() == [32, 6]  # sequence 1 appended, sequence 0 refused
+    changed = (pc.k_pool != before).any(dim=(1, 2, 3)).nonzero().flatten().tolist()
+    assert changed == [int(pc.host_table[1, 0])]  # only sequence 1's page was written
+    with pytest.raises(ValueError, match="unmapped"):
+        pc.check_errors()
+    pc.check_errors()  # the flag was reset
+
+
 @pytest.mark.parametrize("kv_heads,mode", [(8, "polar"), (2, "polar"), (8, "dense")])
 def test_engine_step_paged_equals_contiguous(kv_heads, mode):
     """The decode engine over paged caches (scattered pages, separate paged
@@ -120,8 +141,8 @@ def test_engine_step_paged_equals_contiguous(kv_heads, mode):
     from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy
     from paper_2505_14884_b200.model import DeviceModel, TransformerConfig
 
-    cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 288, "relu")
-    model = DeviceModel.from_host(cfg, po.random_model(2, 256, 1024, 8, kv_heads, 512, 288, seed=21))
+    cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 400, "relu")
+    model = DeviceModel.from_host(cfg, po.random_model(2, 256, 1024, 8, kv_heads, 512, 400, seed=21))
     polar = mode == "polar"
     pol = SparsityPolicy(mode=mode, mlp_k_table={0: 128, 1: 128} if polar else None,
                          head_density=0.5 if polar else 1.0)
@@ -129,24 +150,59 @@ def test_engine_step_paged_equals_contiguous(kv_heads, mode):
     mr = [pb.MlpRouter(256, 1024, seed=30 + e) for e in range(2)]
     engs = []
     for pr, rv in ((0, "full"), (128, "full"), (128, "on_demand")):  # head_dim 32: the SHA tile is 128 rows
-        e = DecodeEngine(model, 8, 288, pol, head_routers=hr, mlp_routers=mr, kv_page_rows=pr, kv_reserve=rv)
+        e = DecodeEngine(model, 8, 400, pol, head_routers=hr, mlp_routers=mr, kv_page_rows=pr, kv_reserve=rv)
         rng = np.random.default_rng(22)
         for c in e.caches:
             c.fill_random(rng, 252)
         engs.append(e)
     assert engs[1].paged and not engs[0].paged
+    # an eager contiguous engine whose recorded selections force the oracle
+    ref_eng = DecodeEngine(model, 8, 400, pol, head_routers=hr, mlp_routers=mr)
+    rng = np.random.default_rng(22)
+    for c in ref_eng.caches:
+        c.fill_random(rng, 252)
+    host = po.random_model(2, 256, 1024, 8, kv_heads, 512, 400, seed=21)
+    rng = np.random.default_rng(22)
+    ocaches = []
+    for _ in range(2):
+        c = po.KVCache(8, kv_heads, 400, 32)
+        c.fill_random(rng, 252)
+        ocaches.append(c)
+    routers = [po.init_mlp_router(256, 1024, seed=30 + e) for e in range(2)]
+
+    def oracle_step(tokens):
+        ref_eng.record = {}
+        eager = ref_eng.step(tokens).clone()
+        rec = ref_eng.record
+        forced = {"heads": {}, "union": {}}
+        if polar:
+            forced["heads"][1] = rec["heads"][0].cpu().numpy()
+            forced["union"] = {e: rec["union"][e].cpu().numpy() for e in range(2)}
+        ref = po.decode_step(host, ocaches, tokens, mode=mode, head_density=pol.head_density,
+                             k_table=pol.mlp_k_table, head_routers=[None, None], mlp_routers=routers, forced=forced)
+        return eager, ref
+
+    def rel(a, b):
+        a = a.cpu().numpy().astype(np.float64)
+        return np.linalg.norm(a - b) / np.linalg.norm(b)
+
     tokens = np.random.default_rng(1).integers(0, 512, 8)
     for _ in range(2):
         outs = [e.step(tokens).clone() for e in engs]
+        eager, ref = oracle_step(tokens)
         assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+        assert rel(outs[0], ref) <= 2e-2
     for e in engs:
         e.capture()
     assert (engs[2].caches[1].host_table >= 0).sum() == 2 * 8  # on demand: only pages 0-1 so far
-    for _ in range(3):  # crosses the 256-row page boundary (252 + 5 steps)
+    for _ in range(140):  # 254 -> 394 rows: past the 256-row page and > 1 SHA tile past the capture window
         outs = [e.step(tokens).clone() for e in engs]
+        eager, ref = oracle_step(tokens)
         assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
-    assert engs[1].caches[1].lengths.cpu().tolist() == [257] * 8
-    assert (engs[2].caches[1].host_table >= 0).sum() == 3 * 8  # page 2 mapped when the appends entered it
+        assert torch.allclose(outs[0], eager, rtol=1e-3, atol=1e-4)
+        assert rel(outs[0], ref) <= 2e-2
+    assert engs[1].caches[1].lengths.cpu().tolist() == [394] * 8
+    assert (engs[2].caches[1].host_table >= 0).sum() == 4 * 8  # pages 2-3 mapped as the appends entered them
 
 
 def test_head_router_fused_append_into_pages():

@@ -474,3 +474,37 @@ def test_small_batch_gemv_up_matches_tiles_and_torch(N):
         assert (got - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
     # the two summation orders differ by at most ~1 bf16 ulp of the output
     assert (g[:, :count].float() - tl[:, :count].float()).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
+
+
+def test_single_unit_references_on_device(golden):
+    """OnlineSoftmaxState / online_softmax_attention (kernels.py:138-210),
+    naive_softmax_attention_single_head and matmul (tensors.py:29-113): the
+    device float64 reference paths match the reference's goldens, and the
+    SHA kernel agrees with them on the same unit (block-size invariance)."""
+    for i in range(int(golden["unit_n"])):
+        q, k, v = golden[f"unit_q_{i}"], golden[f"unit_k_{i}"], golden[f"unit_v_{i}"]
+        d_h = q.shape[0]
+        scale = 1.0 / math.sqrt(d_h)
+        bs = int(golden[f"unit_bs_{i}"])
+        naive = pb.naive_softmax_attention_single_head(q, k, v, scale)
+        assert naive.is_cuda and naive.dtype == torch.float32
+        np.testing.assert_allclose(naive.cpu().numpy(), golden[f"unit_naive_{i}"], rtol=1e-5, atol=1e-6)
+        for variant in ("running", "deferred"):
+            out, st = pb.online_softmax_attention(q, k, v, scale, pb.FlashBlockParams(bs), variant)
+            np.testing.assert_allclose(out.cpu().numpy(), golden[f"unit_online_{variant}_{i}"], rtol=1e-5,
+                                       atol=1e-6)
+            np.testing.assert_allclose([st.l_acc, st.m_acc], golden[f"unit_state_{variant}_{i}"], rtol=1e-9)
+        # the SHA kernel on the same single unit (B = 1, one head)
+        n = k.shape[0]
+        cache = pb.KVCache(1, 1, n, d_h)
+        cache.keys[0, 0] = torch.from_numpy(k).cuda().bfloat16()
+        cache.values[0, 0] = torch.from_numpy(v).cuda().bfloat16()
+        cache.set_lengths([n])
+        sha = pb.selective_head_flash_attention_decode(q.reshape(1, 1, 1, d_h), cache, pb.BatchHeadIndex([[0]]))
+        assert np.abs(sha.cpu().numpy().reshape(d_h) - golden[f"unit_naive_{i}"]).max() <= 2e-2
+    with pytest.raises(pb.EmptyCacheError):
+        pb.naive_softmax_attention_single_head(np.ones(8), np.ones((0, 8)), np.ones((0, 8)), 1.0)
+    got = pb.matmul(golden["matmul_a"], golden["matmul_b"])
+    np.testing.assert_allclose(got.cpu().numpy(), golden["matmul_out"], rtol=1e-6, atol=1e-6)
+    with pytest.raises(ValueError):
+        pb.matmul(np.ones((2, 3)), np.ones((4, 2)))

@@ -163,3 +163,20 @@ def test_decode_step_matches_reference(golden, tag, kv_heads, mode):
         if mode == "polar":
             assert np.array_equal(rec["union"][ell], golden[f"dec_{tag}_{mode}_union_{ell}"])
     assert np.array_equal(logits, golden[f"dec_{tag}_{mode}_logits"])
+
+
+def test_single_unit_references(golden):
+    """kernels.py:138-210 (OnlineSoftmaxState / online_softmax_attention) and
+    tensors.py:83-113 (naive_softmax_attention_single_head), both variants."""
+    for i in range(int(golden["unit_n"])):
+        q, k, v = golden[f"unit_q_{i}"], golden[f"unit_k_{i}"], golden[f"unit_v_{i}"]
+        scale = 1.0 / math.sqrt(q.shape[0])
+        bs = int(golden[f"unit_bs_{i}"])
+        np.testing.assert_allclose(po.naive_softmax_attention_single_head(q, k, v, scale),
+                                   golden[f"unit_naive_{i}"], rtol=1e-6, atol=1e-7)
+        for variant in ("running", "deferred"):
+            out, st = po.online_softmax_attention(q, k, v, scale, bs, variant)
+            np.testing.assert_allclose(out, golden[f"unit_online_{variant}_{i}"], rtol=1e-6, atol=1e-7)
+            np.testing.assert_allclose([st.l_acc, st.m_acc], golden[f"unit_state_{variant}_{i}"], rtol=1e-12)
+    np.testing.assert_allclose(po.matmul(golden["matmul_a"], golden["matmul_b"]), golden["matmul_out"],
+                               rtol=1e-6, atol=1e-6)
