@@ -1,33 +1,45 @@
 """Decode throughput benchmark (driver contract: one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config opt-6.7b] [--batch 64] [--ctx 1920] [--rho 0.5] [--union 0.5]
+                    [--config opt-6.7b] [--batch 64] [--ctx 1920] [--rho 0.5]
+                    [--union 0.5] [--k-frac 0.1] [--dp] [--no-extra]
 
-Metric (BASELINE.json): decode tokens/s (polar sparse step) vs the dense
+Metric (BASELINE.json): decode tokens/s of the polar sparse step vs the dense
 step, at the OPT-6.7B shape (configs[1]) by default: random-init weights
 N(0, 0.02), synthetic N(0,1) KV history of ``ctx`` tokens, batch 64, head
-density rho=0.5 (16 of 32 heads from the head router's top-k; layer 0
-dense), union neuron density |S|/D set by a hot-neuron router bias
-(SURVEY.md §7).  A "step" = one full 32-layer decode step (embed -> 32 x
-[LN, QKV, KV append, head router+top-k, SHA, O-proj, LN, MLP router,
-top-k, union, selective MLP] -> LN -> LM head -> argmax), replayed from one
-CUDA graph.  Inputs exceed L2 (64 GB of KV), so no explicit L2 flush.
+density rho = 0.5 (16 of 32 heads from the head router's top-k; layer 0
+dense).  Neuron selection follows the reference's heavy-tailed
+"hot-neuron" recipe (analysis.py:124-140): every token keeps its top
+k = 0.1*D router logits; a fixed hot set (sized so that the batch union
+|S| is ~``--union``*D at B = 64) fires on every token, the remaining picks
+vary token by token, so |S| grows with the batch as in the paper.  A "step"
+= one full decode step (embed -> L x [LN, QKV, KV append, head router +
+top-k, SHA, O-proj, LN, MLP router, top-k, union, selective MLP] -> LN ->
+LM head -> argmax), replayed from one CUDA graph.  Inputs exceed L2
+(tens of GB of KV), so no explicit L2 flush.
 
 * value        -- polar tok/s, device-timed (CUDA events), max over ranks;
-* dense        -- the same kernels at full density (rho=1, every neuron);
-* e2e          -- the public engine API with HOST token buffers: per step a
-                  pinned H2D copy of the tokens, graph replay, D2H of the next
-                  tokens and a host sync, all inside the timed region;
+* dense        -- the same engine at full density (every head, every
+                  neuron; cuBLAS dense MLP) on the same caches;
+* e2e          -- ``DecodeEngine.step()`` (the public API) with HOST tokens:
+                  per step the pinned H2D copy of the tokens, the graph
+                  replay, the D2H read of the next tokens and a host sync,
+                  all inside the timed region;
 * roofline     -- the SHA kernel (dominant) timed alone on the same caches:
                   algorithmic bytes / CUDA-event duration vs
                   MEASURED_PEAKS.json hbm_gbs;
-* cpu_baseline -- the oracle (numpy port of the reference, f32/f64 on the
-                  host cores) on one decode layer of the same workload, x L.
+* cpu_baseline -- the UNMODIFIED reference package (``sparsedecode``,
+                  installed into baseline/_ref) running its own
+                  ``engine.decode_step`` on one layer of the same workload
+                  on the host cores, x L layers;
+* configs      -- further driver-observed points (other batch sizes, the
+                  LLaMA-3.1-8B shape), each with the byte-model ideal ratio.
 
-``--impl reference`` runs only the reference arm: the oracle port of the
-reference CPU path (there is no GPU reference implementation), rank 0 only.
-N > 1 (torchrun): every rank decodes its own batch (data-parallel replicas,
-weak scaling, no data-path collective).
+``--impl reference`` runs only the reference arm (rank 0; other ranks exit).
+N > 1 (torchrun): tensor parallelism over the ranks on the same workload
+(one global batch, heads + neurons sharded, routers replicated, NCCL
+all-reduce of bf16 partials after the O- and down-projections; strong
+scaling); ``--dp`` runs independent data-parallel replicas instead.
 """
 
 from __future__ import annotations
@@ -36,6 +48,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -45,9 +58,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -57,15 +71,19 @@ def parse():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--ctx", type=int, default=1920)
     ap.add_argument("--rho", type=float, default=0.5)
-    ap.add_argument("--union", type=float, default=0.5, help="target |S|/D of the MLP union")
+    ap.add_argument("--union", type=float, default=0.5, help="target |S|/D of the MLP union at batch 64")
+    ap.add_argument("--k-frac", type=float, default=0.1, help="per-token neuron budget k / D")
+    ap.add_argument("--union-recipe", default="hot-cold", choices=["hot-cold", "hot-set"],
+                    help="hot-cold: per-token top-k over a fixed hot set + varying cold picks (default); "
+                         "hot-set: every token's top-k is exactly the same hot set (k = |S|)")
     ap.add_argument("--kv-ring", type=int, default=0, help="alias KV storage over this many buffers (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
-    ap.add_argument("--tp", action="store_true",
-                    help="tensor parallel over the torchrun ranks (heads + neurons sharded, routers replicated, "
-                         "NCCL all-reduce after the O- and down-projections); default: data-parallel replicas")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra driver-observed configs")
+    ap.add_argument("--dp", action="store_true", help="N > 1: data-parallel replicas instead of TP")
+    ap.add_argument("--tp", action="store_true", help="(default for N > 1) tensor parallelism over the ranks")
     ap.add_argument("--distinct-layers", type=int, default=0,
                     help="TP: distinct weight sets cycled over the layers (0 = all distinct)")
-    ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = same as GPU)")
+    ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = the workload batch)")
     ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
     ap.add_argument("--kv-page-rows", type=int, default=0,
                     help="paged KV caches with this many rows per page (0 = contiguous)")
@@ -73,7 +91,7 @@ def parse():
                     help="paged KV: map every page up front, or each page as the appends enter it")
     ap.add_argument("--concurrent-head-router", action="store_true",
                     help="head router as a concurrent graph branch instead of fused with the KV append")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def load_peaks():
@@ -153,52 +171,175 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# ---------------------------------------------------------------- CPU (oracle) leg
-def cpu_layer_sample(cfg, batch, ctx, rho, union, reps=2, warm=1, seed=0):
-    """One decode layer of the workload on the host with the oracle (numpy
-    restatement of the reference, f32 storage / f64 accumulation); returns
-    seconds per layer (median of ``reps``)."""
-    from oracle import polar_oracle as po
+# ---------------------------------------------------------------- workload recipe
+def hot_cold_hot_set(D: int, k: int, target: float, batch: int = 64) -> int:
+    """Hot-set size of the heavy-tailed neuron recipe (analysis.py:124-140).
 
+    Every token keeps its top k neurons: the n_hot hot ones (a large router
+    bias: they fire on every token, hot_p ~ 1) plus k - n_hot cold picks
+    that vary token by token.  With independent cold picks the expected
+    union over ``batch`` tokens is n_hot + C*(1 - exp(-batch*(k - n_hot)/C)),
+    C = D - n_hot; solve it for |S| = target*D by bisection (the measured
+    union is reported next to every number).
+    """
+    want = target * D
+
+    def union(n):
+        c, C = k - n, D - n
+        return n + C * (1.0 - math.exp(-batch * c / C)) if C > 0 else D
+
+    if union(0) <= want:
+        return 0
+    lo, hi = 0, k
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if union(mid) > want:
+            lo = mid
+        else:
+            hi = mid
+    return hi
+
+
+def neuron_recipe(args, D: int):
+    """(k per token, hot-set size) of the MLP selection."""
+    if args.union_recipe == "hot-set":
+        k = max(1, int(round(args.union * D)))
+        return k, k
+    k = max(1, int(round(args.k_frac * D)))
+    return k, hot_cold_hot_set(D, k, args.union)
+
+
+def workload_config(args, cfg, batch=None, config=None, ctx=None, world=1, tp=False):
+    """The workload keys shared by both arms (GPU-only facts live elsewhere)."""
+    config = config or args.config
+    batch = batch or args.batch
+    ctx = ctx or args.ctx
+    D = cfg.ffn_dim
+    k, n_hot = neuron_recipe(args, D)
+    return {"workload": f"{config} polar decode step", "model_shape": config, "global_batch": batch,
+            "seq_len": ctx, "head_density": args.rho,
+            "neuron_selection": (f"per-token top-{k} (k/D={k / D:.3f}) over a hot set of {n_hot} + per-token "
+                                 f"cold picks (analysis.py:124-140); target |S|/D={args.union} at B=64")
+            if cfg.activation == "relu" else "dense SwiGLU MLP (never sparsified, engine.py:67-70)",
+            "layers": cfg.layers, "d_model": cfg.model_dim, "ffn": cfg.ffn_dim, "heads": cfg.heads,
+            "kv_heads": cfg.kv_heads, "parallelism": (f"tp{world}" if tp else f"dp{world}"),
+            "l2": "inputs larger than L2 (KV cache >> 126 MB); no flush"}
+
+
+# ---------------------------------------------------------------- byte model
+def step_bytes(cfg, B, ctx, k_h, S, dense: bool, tp: int = 1) -> float:
+    """HBM bytes one decode step must move per GPU (bf16 weights and KV):
+    every layer's QKV / O weights, the selected K/V rows, the routers and
+    the gathered MLP rows (polar) or every MLP weight (dense), plus the LM
+    head.  Layer 0 attention is dense in polar mode (SparsityPolicy)."""
+    d, D, H_kv, d_h = cfg.model_dim, cfg.ffn_dim, cfg.kv_heads, cfg.head_dim
+    dk = H_kv * d_h
+    attn_w = (d * (d + 2 * dk) + d * d) * 2 / tp
+    kv_full = B * ctx * H_kv * d_h * 4 / tp
+    total = 0.0
+    for ell in range(cfg.layers):
+        total += attn_w
+        if dense or ell == 0:
+            total += kv_full
+        else:
+            total += kv_full * k_h / H_kv + d * H_kv * 2
+        if cfg.activation == "swiglu":
+            total += 3 * D * d * 2 / tp
+        elif dense:
+            total += 2 * D * d * 2 / tp
+        else:
+            h_r = min(1024, 4 * d)
+            total += (d * h_r + h_r * D) * 2 + 2 * S * d * 2 / tp + B * D * 4
+    total += cfg.vocab * d * 2
+    return total
+
+
+def ideal_ratio(cfg, B, ctx, rho, S):
+    k_h = max(1, math.ceil(rho * cfg.kv_heads - 1e-9))
+    return step_bytes(cfg, B, ctx, k_h, S, True) / step_bytes(cfg, B, ctx, k_h, S, False)
+
+
+# ---------------------------------------------------------------- reference (CPU) leg
+def import_reference():
+    """The unmodified reference package: baseline/_ref (pip-installed from
+    /root/reference, travels to the GPU box), else None."""
+    if REF_DIR not in sys.path and os.path.isdir(os.path.join(REF_DIR, "sparsedecode")):
+        sys.path.insert(0, REF_DIR)
+    try:
+        import sparsedecode  # noqa: F401
+        return sparsedecode
+    except Exception:
+        return None
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        blas = int(max(n)) if n else None
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "cpu_model": model, "blas_threads": blas}
+
+
+def reference_layer_sample(args, cfg, batch, reps=2, warm=1, seed=0):
+    """One polar decode layer of the workload through the reference's own
+    ``engine.decode_step`` (a 1-layer model of the same shape, vocab 512 so
+    the LM head is negligible, layer-0 attention routed like every other
+    layer).  Returns (seconds per layer, kind, sample text); falls back to
+    the oracle port only if the reference package is not importable."""
     rng = np.random.default_rng(seed)
     d, D, H, H_kv, d_h = cfg.model_dim, cfg.ffn_dim, cfg.heads, cfg.kv_heads, cfg.head_dim
-    dk = H_kv * d_h
-    g = lambda *s: rng.standard_normal(s, dtype=np.float32) * np.float32(0.02)  # noqa: E731
-    lw = dict(ln1_g=np.ones(d, np.float32), ln1_b=np.zeros(d, np.float32), w_q=g(d, d), b_q=np.zeros(d, np.float32),
-              w_k=g(d, dk), b_k=np.zeros(dk, np.float32), w_v=g(d, dk), b_v=np.zeros(dk, np.float32),
-              w_o=g(d, d), b_o=np.zeros(d, np.float32), ln2_g=np.ones(d, np.float32),
-              ln2_b=np.zeros(d, np.float32), mlp_w1=g(d, D), mlp_b1=g(D), mlp_w2=g(d, D),
-              mlp_b2=np.zeros(d, np.float32))
-    h_r = min(1024, 4 * d)
-    hr = {"w": rng.standard_normal((d, H_kv)) / math.sqrt(d), "b": np.zeros(H_kv)}
-    mr = {"w_in": rng.standard_normal((d, h_r), dtype=np.float32) * np.float32(math.sqrt(2 / d)),
-          "b_in": np.zeros(h_r), "w_out": rng.standard_normal((h_r, D), dtype=np.float32) * np.float32(math.sqrt(2 / h_r)),
-          "b_out": np.zeros(D)}
-    k_mlp = max(1, int(union * D))
-    hot = rng.choice(D, k_mlp, replace=False)
-    mr["b_out"][hot] += 20.0
-    cache = po.KVCache(batch, H_kv, ctx + warm + reps + 1, d_h)
-    cache.fill_random(rng, ctx)
-    x = rng.standard_normal((batch, d), dtype=np.float32)
-    k_h = po.head_budget(rho, H_kv)
-    scale = 1.0 / math.sqrt(d_h)
+    relu = cfg.activation == "relu"
+    k, n_hot = neuron_recipe(args, D)
+    cap = args.ctx + warm + reps + 2
+    sd = import_reference()
+    if sd is not None:
+        from sparsedecode import engine as sde, model as sdm
+        c1 = sdm.TransformerConfig(1, d, D, H, H_kv, 512, cap, cfg.activation)
+        model = sdm.random_model(c1, seed)
+        cache = sd.KVCache(batch, H_kv, cap, d_h)
+        cache.fill_random(rng, args.ctx)
+        hr = [sd.HeadRouter(d, H_kv, seed=100)]
+        mr = None
+        table = None
+        if relu:
+            mr = [sd.MlpRouter(d, D, seed=200)]
+            mr[0].b_out_[rng.choice(D, n_hot, replace=False)] += 20.0
+            table = sd.LayerKTable(((0, k, 1.0),))
+        policy = sd.SparsityPolicy(mode="polar", mlp_k_table=table, head_density=args.rho,
+                                   layer0_dense_attention=False)
+        sess = sd.DecodeSession(caches=[cache], policy=policy, mlp_routers=mr, head_routers=hr)
 
-    def layer():
-        h1 = po.layernorm(x, lw["ln1_g"], lw["ln1_b"])
-        q4 = (po.matmul(h1, lw["w_q"]) + lw["b_q"]).reshape(batch, H, d_h)[:, :, None, :]
-        kk = (po.matmul(h1, lw["w_k"]) + lw["b_k"]).reshape(batch, H_kv, d_h)
-        vv = (po.matmul(h1, lw["w_v"]) + lw["b_v"]).reshape(batch, H_kv, d_h)
-        cache.append_step(kk, vv)
-        sel = po.topk_indices_rows(po.head_router_forward(hr["w"], hr["b"], h1), k_h)
-        attn = po.gqa_selective_attention_decode(q4, cache, sel, 64, scale)
-        x2 = x + (po.matmul(attn[:, :, 0, :].reshape(batch, d), lw["w_o"]) + lw["b_o"])
-        h2 = po.layernorm(x2, lw["ln2_g"], lw["ln2_b"])
-        logits = po.mlp_router_forward(mr["w_in"], mr["b_in"], mr["w_out"], mr["b_out"], h2)
-        union_idx = po.union_neuron_indices(list(po.topk_indices_rows(logits, k_mlp)))
-        y = po.sparse_mlp_forward(h2[:, None, :], lw["mlp_w1"], lw["mlp_b1"], lw["mlp_w2"], lw["mlp_b2"],
-                                  union_idx)
-        return x2 + y[:, 0, :]
+        def layer():
+            sde.decode_step(sess, model, rng.integers(0, 512, batch))
+        kind, what = "reference", "sparsedecode.engine.decode_step (unmodified reference, baseline/_ref)"
+    else:
+        from oracle import polar_oracle as po
+        host = po.random_model(1, d, D, H, H_kv, 512, cap, cfg.activation, seed=seed)
+        cache = po.KVCache(batch, H_kv, cap, d_h)
+        cache.fill_random(rng, args.ctx)
+        mrs = None
+        if relu:
+            mrs = [po.init_mlp_router(d, D, seed=200)]
+            mrs[0]["b_out"][rng.choice(D, n_hot, replace=False)] += 20.0
+        hrs = [po.init_head_router(d, H_kv, seed=100)]
 
+        def layer():
+            po.decode_step(host, [cache], rng.integers(0, 512, batch), mode="polar", head_density=args.rho,
+                           layer0_dense=False, k_table={0: k} if relu else None, head_routers=hrs,
+                           mlp_routers=mrs)
+        kind, what = "port", "oracle/polar_oracle.py decode_step (numpy port; reference not importable)"
     for _ in range(warm):
         layer()
     ts = []
@@ -206,19 +347,13 @@ def cpu_layer_sample(cfg, batch, ctx, rho, union, reps=2, warm=1, seed=0):
         t0 = time.perf_counter()
         layer()
         ts.append(time.perf_counter() - t0)
-    return float(np.median(ts))
+    t = float(np.median(ts))
+    sample = (f"{what}: one decode layer of {args.config} at B={batch}, ctx {args.ctx}, rho {args.rho}, "
+              f"per-token top-{k if relu else 0} neurons, median of {reps} after {warm} warm-up, x {cfg.layers} "
+              f"layers (embed / LM head excluded)")
+    return t, kind, sample
 
 
-def cpu_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
-        return int(max(n)) if n else os.cpu_count()
-    except Exception:
-        return os.cpu_count()
-
-
-# ---------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -227,22 +362,20 @@ def run_reference(args):
 
     cfg = SHAPES[args.config]
     batch = args.cpu_batch or args.batch
-    per_layer = []
-    # each "step" = one decode layer timed on the host, x L layers
     t_setup = time.perf_counter()
-    s = cpu_layer_sample(cfg, batch, args.ctx, args.rho, args.union, reps=args.steps, warm=min(args.warmup, 3))
-    per_layer.append(s)
+    reps = max(1, min(args.steps, 3))
+    s, kind, sample = reference_layer_sample(args, cfg, batch, reps=reps, warm=min(args.warmup, 1))
     step_s = s * cfg.layers
     value = batch / step_s
-    sample = (f"oracle port of the reference (numpy f32/f64), one decode layer of {args.config} "
-              f"B={batch} ctx={args.ctx} rho={args.rho} |S|/D={args.union}, median of {args.steps} "
-              f"(after {min(args.warmup, 3)} warm-up), x {cfg.layers} layers")
+    info = cpu_info()
     line = {"impl": "reference", "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
-            "data": "synthetic", "config": workload_config(args, cfg),
-            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cpu_threads(), "kind": "port",
-                             "sample": sample},
+            "higher_is_better": True, "scaling": "weak" if (args.gpus == 1 or args.dp) else "strong",
+            "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+            "config": workload_config(args, cfg, world=args.gpus, tp=args.gpus > 1 and not args.dp),
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": info["blas_threads"] or info["cpu_count"],
+                             "kind": kind, "sample": sample + (f" (batch {batch} of {args.batch}: tok/s per "
+                                                               f"host-step scales with the batch)"), **info},
             "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t_setup}
     print(json.dumps(line), flush=True)
@@ -251,27 +384,19 @@ def run_reference(args):
 def ncu_traffic(kernel, args):
     """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel`
     from the committed `ncu --set full` capture of this same workload
-    (tools/gpu_profiles.sh -> profiles/r01_ncu_traffic.json), else None."""
-    if (args.config, args.batch, args.ctx, args.rho, args.union) != ("opt-6.7b", 64, 1920, 0.5, 0.5):
-        return None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            doc = json.load(f)
-        for k in doc["kernels"]:
-            if kernel in k["kernel"]:
-                return k["dram_read_bytes"] + k["dram_write_bytes"]
-    except Exception:
-        return None
-    return None
-
-
-def workload_config(args, cfg):
-    return {"workload": f"{args.config} polar decode step", "model_shape": args.config, "global_batch": args.batch,
-            "seq_len": args.ctx, "head_density": args.rho, "union_density": args.union,
-            "layers": cfg.layers, "d_model": cfg.model_dim, "ffn": cfg.ffn_dim, "heads": cfg.heads,
-            "kv_heads": cfg.kv_heads, "parallelism": f"dp{args.gpus}",
-            "kv_layout": f"paged ({args.kv_page_rows} rows/page)" if args.kv_page_rows else "contiguous",
-            "l2": "inputs larger than L2 (KV cache >> 126 MB); no flush"}
+    (profiles/r02_ncu_traffic.json), else None."""
+    if (args.config, args.batch, args.ctx, args.rho) != ("opt-6.7b", 64, 1920, 0.5):
+        return None, None
+    for name in ("r02_ncu_traffic.json", "r01_ncu_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                doc = json.load(f)
+            for k in doc["kernels"]:
+                if kernel in k["kernel"]:
+                    return k["dram_read_bytes"] + k["dram_write_bytes"], f"profiles/{name}"
+        except Exception:
+            continue
+    return None, None
 
 
 # ---------------------------------------------------------------- our arm
@@ -279,6 +404,91 @@ def sha_algorithmic_bytes(lengths, k_h, G, d_h, B, H):
     """selected K+V rows + Q + O (zeros included) + ids + lengths."""
     kv = float(np.sum(lengths)) * k_h * d_h * 2 * 2
     return kv + B * k_h * G * d_h * 2 + B * H * d_h * 2 + B * k_h * 4 + B * 4
+
+
+class Setup:
+    """Engines (polar + dense on shared caches) for one workload point."""
+
+    def __init__(self, args, config, B, ctx, dev, world, rank, tp_on, steps, warmup, model=None):
+        import torch
+
+        import paper_2505_14884_b200 as pb
+        from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy
+        from paper_2505_14884_b200.model import SHAPES, DeviceModel
+
+        self.cfg = cfg = SHAPES[config]
+        self.B, self.ctx = B, ctx
+        L, H_kv, d_h, D = cfg.layers, cfg.kv_heads, cfg.head_dim, cfg.ffn_dim
+        self.cap = cap = ctx + warmup * 2 + steps * 3 + 16
+        free = torch.cuda.mem_get_info(dev)[0]
+        self.tp = None
+        if tp_on:
+            from paper_2505_14884_b200.parallel import TPPlan, TensorParallel, random_shard
+
+            plan = TPPlan.make(cfg, world, rank)
+            self.tp = TensorParallel(plan)
+            self.model = model or random_shard(cfg, plan, seed=1234, device=dev,
+                                               distinct_layers=args.distinct_layers or None)
+            self.H_loc, self.Hkv_loc, self.D_loc = plan.heads_local, plan.kv_heads_local, plan.ffn_local
+        else:
+            self.model = model or DeviceModel.random(cfg, seed=1234 + rank, device=dev)
+            self.H_loc, self.Hkv_loc, self.D_loc = cfg.heads, H_kv, D
+        kv_layer = B * self.Hkv_loc * cap * d_h * 2 * 2
+        budget = free - (0 if model is not None else self.model.weight_bytes()) - 14 * 2 ** 30
+        ring = args.kv_ring or (L if kv_layer * L <= budget else max(2, int(budget // kv_layer)))
+        self.ring = min(ring, L)
+        self.k_h = math.ceil(args.rho * H_kv - 1e-9)
+        self.relu = cfg.activation == "relu"
+        k, n_hot = neuron_recipe(args, D)
+        self.k_mlp, self.n_hot = k, n_hot
+        gen = np.random.default_rng(7)  # same on every TP rank: routers are replicated
+        hr = [pb.HeadRouter(cfg.model_dim, H_kv, seed=100 + ell, device=dev) for ell in range(L)]
+        mr = None
+        if self.relu:
+            mr = [pb.MlpRouter.random_device(cfg.model_dim, D, seed=200 + ell, device=dev,
+                                             hot=gen.choice(D, n_hot, replace=False) if n_hot else None)
+                  for ell in range(L)]
+        polar = SparsityPolicy(mode="polar", head_density=args.rho,
+                               mlp_k_table={ell: k for ell in range(L)} if self.relu else None)
+        self.eng = DecodeEngine(self.model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=self.ring,
+                                router_backend=args.router_backend, concurrent_router=args.concurrent_head_router,
+                                tp=self.tp, kv_page_rows=args.kv_page_rows, kv_reserve=args.kv_reserve)
+        self.eng.fill_random(ctx, seed=99 + (0 if tp_on else rank))
+        self.dense = DecodeEngine(self.model, B, cap, SparsityPolicy(mode="dense"), caches=self.eng.caches,
+                                  tp=self.tp)
+        self.tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32,
+                                         generator=torch.Generator().manual_seed(5)).pin_memory()
+        self.graphs, self.graph_error = True, None
+        self.eng.tokens.copy_(self.tokens_host)
+        self.dense.tokens.copy_(self.tokens_host)
+        try:
+            self.eng.capture()
+            self.dense.capture()
+        except Exception as exc:  # reported in the JSON line (TP collectives that cannot be captured)
+            if self.tp is None:
+                raise
+            self.graphs, self.graph_error = False, f"{type(exc).__name__}: {exc}"[:200]
+            self.eng.graph = self.dense.graph = None
+
+    def union_density(self):
+        """Mean over layers of the device union size / D (after timing)."""
+        if not self.relu:
+            return None
+        c = self.eng.union_counts.float()
+        if self.tp is not None and self.tp.plan.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(c)  # each rank holds the count of its neuron shard
+        return float(c.mean().item()) / self.cfg.ffn_dim
+
+
+def replay(engine):
+    def f():
+        if engine.graph is not None:
+            engine.graph.replay()
+        else:
+            engine.step_launches()
+        engine._advance()
+    return f
 
 
 def run_ours(args):
@@ -289,68 +499,13 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    tp_on = (world > 1 and not args.dp) or args.tp
 
     import paper_2505_14884_b200 as pb
-    from paper_2505_14884_b200 import _lib, kernels as pk
-    from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy
-    from paper_2505_14884_b200.model import SHAPES, DeviceModel
-
-    cfg = SHAPES[args.config]
-    B, ctx = args.batch, args.ctx
-    L, H, H_kv, d_h, D = cfg.layers, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.ffn_dim
-    cap = ctx + args.warmup * 2 + args.steps * 3 + 8
-    free = torch.cuda.mem_get_info(dev)[0]
-    tp = None
-    if args.tp:
-        # every rank holds KV groups [r*H_kv/T, ...) + their heads and neurons
-        # [r*D/T, ...); routers are replicated (identical seeds on all ranks)
-        from paper_2505_14884_b200.parallel import TPPlan, TensorParallel, random_shard
-
-        plan = TPPlan.make(cfg, world, rank)
-        tp = TensorParallel(plan)
-        model = random_shard(cfg, plan, seed=1234, device=dev, distinct_layers=args.distinct_layers or None)
-        H_loc, Hkv_loc, D_loc = plan.heads_local, plan.kv_heads_local, plan.ffn_local
-    else:
-        model = DeviceModel.random(cfg, seed=1234 + rank, device=dev)
-        H_loc, Hkv_loc, D_loc = H, H_kv, D
-    kv_layer = B * Hkv_loc * cap * d_h * 2 * 2
-    budget = free - model.weight_bytes() - 12 * 2 ** 30
-    ring = args.kv_ring or (L if kv_layer * L <= budget else max(2, int(budget // kv_layer)))
-    ring = min(ring, L)
-
-    k_h = math.ceil(args.rho * H_kv - 1e-9)
-    k_mlp = max(1, int(round(args.union * D)))
-    gen = np.random.default_rng(7 + (0 if tp is not None else rank))
-    sparse_relu = cfg.activation == "relu"
-    hr = [pb.HeadRouter(cfg.model_dim, H_kv, seed=100 + ell, device=dev) for ell in range(L)]
-    mr = None
-    if sparse_relu:
-        mr = [pb.MlpRouter.random_device(cfg.model_dim, D, seed=200 + ell, device=dev,
-                                         hot=gen.choice(D, k_mlp, replace=False)) for ell in range(L)]
-    polar = SparsityPolicy(mode="polar", head_density=args.rho,
-                           mlp_k_table={ell: k_mlp for ell in range(L)} if sparse_relu else None)
-    eng = DecodeEngine(model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=ring,
-                       router_backend=args.router_backend, concurrent_router=args.concurrent_head_router, tp=tp,
-                       kv_page_rows=args.kv_page_rows, kv_reserve=args.kv_reserve)
-    eng.fill_random(ctx, seed=99 + rank)
-    dense = DecodeEngine(model, B, cap, SparsityPolicy(mode="dense"), caches=eng.caches, tp=tp)
-    tokens_host = torch.randint(0, cfg.vocab, (B,), dtype=torch.int32).pin_memory()
-    out_host = torch.empty(B, dtype=torch.int64).pin_memory()
-    eng.tokens.copy_(tokens_host)
-    dense.tokens.copy_(tokens_host)
-    graphs = True
-    try:
-        eng.capture()
-        dense.capture()
-    except Exception as exc:  # e.g. a collective that cannot be captured: time eager steps
-        if tp is None:
-            raise
-        graphs = False
-        eng.graph = dense.graph = None
-        print(f"[bench] TP step not graph-capturable ({type(exc).__name__}); timing eager steps", file=sys.stderr)
+    from paper_2505_14884_b200 import kernels as pk
 
     def barrier():
         if world > 1:
@@ -372,16 +527,9 @@ def run_ours(args):
             ms = float(t.item())
         return ms
 
-    def replay(engine):
-        def f():
-            if engine.graph is not None:
-                engine.graph.replay()
-            else:
-                engine.step_launches()
-            engine._advance()
-        return f
-
-    # warm-up
+    su = Setup(args, args.config, args.batch, args.ctx, dev, world, rank, tp_on, args.steps, args.warmup)
+    cfg, B, eng, dense = su.cfg, su.B, su.eng, su.dense
+    L, H, H_kv, d_h, D = cfg.layers, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.ffn_dim
     for _ in range(args.warmup):
         replay(dense)()
         replay(eng)()
@@ -390,20 +538,32 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         ms_polar = timed(replay(eng), args.steps)
     clocks = clk.summary()
+    union_density = su.union_density()
 
-    # union density actually used (device count of the last layer, read after timing)
-    union_density = None
-    if sparse_relu:
-        union_density = int(eng.union_count.item()) / D
-
-    # e2e: host tokens in, host next-tokens out, through the engine API
-    def e2e_step():
-        eng.tokens.copy_(tokens_host, non_blocking=True)
-        if eng.graph is not None:
-            eng.graph.replay()
+    # per-rank load (TP): selected KV groups and union neurons owned by this rank
+    load = None
+    if su.tp is not None:
+        lo = su.tp.group_base
+        sel = eng.sel[:, :su.k_h]
+        heads_mine = float(((sel >= lo) & (sel < lo + su.Hkv_loc)).sum().item())
+        neurons_mine = float(eng.union_counts.float().mean().item()) if su.relu else 0.0
+        t = torch.tensor([heads_mine, neurons_mine], device=dev)
+        if world > 1:
+            allv = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allv, t)
+            allv = torch.stack(allv).cpu().numpy()
         else:
-            eng.step_launches()
-        eng._advance()
+            allv = t[None].cpu().numpy()
+        load = {"selected_kv_units_per_rank": allv[:, 0].tolist(),
+                "union_neurons_per_rank": allv[:, 1].tolist(),
+                "units_max_over_mean": float(allv[:, 0].max() / max(1e-9, allv[:, 0].mean())),
+                "neurons_max_over_mean": float(allv[:, 1].max() / max(1e-9, allv[:, 1].mean())) if su.relu else None}
+
+    # e2e: the public API (DecodeEngine.step) with host tokens in / next tokens out
+    out_host = torch.empty(B, dtype=torch.int64).pin_memory()
+
+    def e2e_step():
+        eng.step(su.tokens_host)
         out_host.copy_(eng.next_tokens, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
@@ -416,24 +576,24 @@ def run_ours(args):
 
     # roofline: the SHA kernel alone on the same caches, one launch per layer
     qkv = eng.qkv
-    k_loc = max(1, min(k_h, Hkv_loc))
-    sel = torch.stack([torch.randperm(Hkv_loc, device=dev)[:k_loc].sort().values for _ in range(B)]).to(torch.int32)
-    dq = H_loc * d_h
+    k_loc = max(1, min(su.k_h, su.Hkv_loc))
+    g = torch.Generator(device=dev).manual_seed(3)
+    sel = torch.stack([torch.randperm(su.Hkv_loc, device=dev, generator=g)[:k_loc].sort().values
+                       for _ in range(B)]).to(torch.int32)
+    dq = su.H_loc * d_h
     out = torch.empty(B, dq, dtype=torch.bfloat16, device=dev)
     lens = [c.host_lengths.copy() for c in eng.caches]
     for c in eng.caches[:2]:
-        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H_loc, eng.scale, out, dq,
+        pk.sha_decode_into(qkv, qkv.shape[1], c, sel, su.H_loc, eng.scale, out, dq,
                            max_len_hint=int(c.host_lengths.max()))
     torch.cuda.synchronize()
-    # one launch per layer captured in a CUDA graph (no host launch overhead
-    # between them), timed with events on the replay stream: median of 3
     sha_graph = torch.cuda.CUDAGraph()
     cap_stream = torch.cuda.Stream(device=dev)
     cap_stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(cap_stream):
         with torch.cuda.graph(sha_graph, stream=cap_stream):
             for c in eng.caches:
-                pk.sha_decode_into(qkv, qkv.shape[1], c, sel, H_loc, eng.scale, out, dq,
+                pk.sha_decode_into(qkv, qkv.shape[1], c, sel, su.H_loc, eng.scale, out, dq,
                                    max_len_hint=int(c.host_lengths.max()))
     torch.cuda.current_stream().wait_stream(cap_stream)
     sha_graph.replay()
@@ -448,75 +608,116 @@ def run_ours(args):
         torch.cuda.synchronize()
         sha_runs.append(s_ev.elapsed_time(e_ev) / L)
     sha_ms = float(np.median(sha_runs))
-    sha_bytes = float(np.mean([sha_algorithmic_bytes(l, k_loc, H // H_kv, d_h, B, H_loc) for l in lens]))
+    sha_bytes = float(np.mean([sha_algorithmic_bytes(l, k_loc, H // H_kv, d_h, B, su.H_loc) for l in lens]))
     hbm_peak, _, peak_kind = load_peaks()
     achieved = sha_bytes / (sha_ms * 1e-3) / 1e9
-    traffic = ncu_traffic("sha_mma_kernel", args)
+    traffic, traffic_src = ncu_traffic("sha_mma_kernel", args)
 
-    # selective MLP kernels alone (UP + DOWN gathered GEMMs), one per layer
-    mlp_ms = None
-    mlp_bytes = None
-    if sparse_relu:
+    # selective MLP kernels alone (UP + DOWN gathered GEMMs), one pair per
+    # layer, over the union the polar step actually produced (last layer)
+    mlp = None
+    if su.relu:
         x2 = torch.randn(B, cfg.model_dim, device=dev).to(torch.bfloat16)
         y = torch.empty(B, cfg.model_dim, dtype=torch.float32, device=dev)
-        k_loc_mlp = min(k_mlp, D_loc)
-        hot_idx = torch.from_numpy(np.sort(gen.choice(D_loc, k_loc_mlp, replace=False))).to(dev, torch.int32)
-        nit = pb.NeuronIndexTensor(0, hot_idx, validate=False)
+        cnt = eng.union_counts[L - 1:L].clone()
+        S = int(cnt.item())
+        idx = eng.union_idx.clone()
         hidden = eng.hidden
-        pk.mlp_into(model.layers[0].mlp, x2, nit.buffer, nit.count, hidden, y)
+        pk.mlp_into(su.model.layers[0].mlp, x2, idx, cnt, hidden, y, expected=S)
         torch.cuda.synchronize()
         mlp_graph = torch.cuda.CUDAGraph()
         cap_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cap_stream):
             with torch.cuda.graph(mlp_graph, stream=cap_stream):
-                for lw in model.layers:
-                    pk.mlp_into(lw.mlp, x2, nit.buffer, nit.count, hidden, y)
+                for lw in su.model.layers:
+                    pk.mlp_into(lw.mlp, x2, idx, cnt, hidden, y, expected=S)
         torch.cuda.current_stream().wait_stream(cap_stream)
         mlp_graph.replay()
         torch.cuda.synchronize()
-        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s_ev.record(st)
-        mlp_graph.replay()
-        e_ev.record(st)
-        torch.cuda.synchronize()
-        mlp_ms = s_ev.elapsed_time(e_ev) / L
-        mlp_bytes = (2 * k_loc_mlp * cfg.model_dim * 2 + k_loc_mlp * 4 + cfg.model_dim * 4 + 2 * B * cfg.model_dim * 2
-                     + k_loc_mlp * 4)
+        runs = []
+        for _ in range(3):
+            s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_ev.record(st)
+            mlp_graph.replay()
+            e_ev.record(st)
+            torch.cuda.synchronize()
+            runs.append(s_ev.elapsed_time(e_ev) / L)
+        mlp_ms = float(np.median(runs))
+        mlp_bytes = 2 * S * cfg.model_dim * 2 + S * 2 + cfg.model_dim * 4 + 2 * B * cfg.model_dim * 2 + S * 4
+        mlp = {"sparse_mlp_us_per_layer": mlp_ms * 1e3, "sparse_mlp_GBps": mlp_bytes / (mlp_ms * 1e-3) / 1e9,
+               "sparse_mlp_frac": mlp_bytes / (mlp_ms * 1e-3) / 1e9 / hbm_peak, "union_size": S,
+               "union_density": S / su.D_loc}
+    n_launch = int(eng.launches_per_step)
+    toks = (1 if su.tp is not None else world) * B * args.steps
+    value = toks / (ms_polar * 1e-3)
+    dense_value = toks / (ms_dense * 1e-3)
+    S_meas = (union_density or 0.0) * D if su.relu else D
+    main_ideal = ideal_ratio(cfg, B, args.ctx, args.rho, S_meas)
+    setup_info = {"kv_storage_buffers": su.ring, "graph_captured": su.graphs, "graph_error": su.graph_error,
+                  "kv_aliasing": ("none" if su.ring == L else f"K/V storage aliased over {su.ring} buffers"),
+                  "hot_set": su.n_hot, "k_per_token": su.k_mlp}
+    del su, eng, dense, sha_graph
+    torch.cuda.empty_cache()
 
-    line = None
+    # further driver-observed points (N = 1 only; same recipe, shorter runs)
+    extra = []
+    if world == 1 and not args.no_extra and args.config == "opt-6.7b":
+        points = [("opt-6.7b", 1), ("opt-6.7b", 16), ("opt-6.7b", 128), ("opt-6.7b", 256),
+                  ("llama-3.1-8b", 64), ("llama-3.1-8b", 512)]
+        ks, kw = min(args.steps, 8), 3
+        for config, b in points:
+            if b == args.batch and config == args.config:
+                continue
+            try:
+                s2 = Setup(args, config, b, args.ctx, dev, world, rank, False, ks, kw)
+                for _ in range(kw):
+                    replay(s2.dense)()
+                    replay(s2.eng)()
+                mp = timed(replay(s2.eng), ks)
+                md = timed(replay(s2.dense), ks)
+                ud = s2.union_density()
+                Sx = (ud or 0.0) * s2.cfg.ffn_dim if s2.relu else s2.cfg.ffn_dim
+                extra.append({"config": config, "global_batch": b, "seq_len": args.ctx, "steps": ks, "warmup": kw,
+                              "value": b * ks / (mp * 1e-3), "dense_value": b * ks / (md * 1e-3),
+                              "speedup_vs_dense": md / mp, "union_density_measured": ud,
+                              "ideal_ratio_byte_model": ideal_ratio(s2.cfg, b, args.ctx, args.rho, Sx),
+                              "kv_storage_buffers": s2.ring})
+                del s2
+            except Exception as exc:  # report, never hide
+                extra.append({"config": config, "global_batch": b, "error": f"{type(exc).__name__}: {exc}"[:200]})
+            torch.cuda.empty_cache()
+
     if rank == 0:
-        toks = (1 if tp is not None else world) * B * args.steps  # TP ranks share one global batch
-        value = toks / (ms_polar * 1e-3)
-        dense_value = toks / (ms_dense * 1e-3)
         cpu = None
         if world == 1 and not args.no_cpu:
             cb = args.cpu_batch or B
-            t_layer = cpu_layer_sample(cfg, cb, ctx, args.rho, args.union, reps=2, warm=1)
-            cpu = {"value": cb / (t_layer * L), "unit": "tok/s", "cores": cpu_threads(), "kind": "port",
-                   "sample": f"oracle (numpy port of the reference path) on one decode layer of the same "
-                             f"workload at B={cb}, median of 2 after 1 warm-up, x {L} layers"}
+            t_layer, kind, sample = reference_layer_sample(args, cfg, cb, reps=2, warm=1)
+            info = cpu_info()
+            cpu = {"value": cb / (t_layer * L), "unit": "tok/s", "cores": info["blas_threads"] or info["cpu_count"],
+                   "kind": kind, "sample": sample, **info}
         line = {
             "metric": "decode_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_polar / args.steps,
-            "higher_is_better": True, "scaling": "strong" if tp is not None else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if tp_on and world > 1 else "weak", "vs_baseline": None,
             "dtype": "bf16",
-            "data": "synthetic (random-init weights N(0,0.02); N(0,1) KV history; hot-neuron router bias)",
-            "config": dict(workload_config(args, cfg), kv_storage_buffers=ring, graph_captured=graphs,
-                           parallelism=f"tp{world}" if tp is not None else f"dp{world}",
-                           kv_aliasing=("none" if ring == L else f"K/V storage aliased over {ring} buffers")),
+            "data": "synthetic (random-init weights N(0,0.02); N(0,1) KV history; hot/cold neuron router bias)",
+            "config": workload_config(args, cfg, world=world, tp=tp_on),
+            "setup": setup_info,
             "dense": {"value": dense_value, "ms_per_step": ms_dense / args.steps},
             "speedup_vs_dense": value / dense_value,
+            "ideal_ratio_byte_model": main_ideal,
             "union_density_measured": union_density,
+            "tp_load": load,
             "e2e": {"value": toks / (ms_e2e * 1e-3), "unit": "tok/s", "h2d_bytes_per_step": B * 4,
-                    "d2h_bytes_per_step": B * 8, "wall_ms_per_step": wall_e2e / args.steps},
-            "gpu_launches": int(eng.launches_per_step) * args.steps,
+                    "d2h_bytes_per_step": B * 8, "wall_ms_per_step": wall_e2e / args.steps,
+                    "api": "DecodeEngine.step(host tokens) + D2H of next tokens + sync"},
+            "gpu_launches": n_launch * args.steps,
             "roofline": {"bound": "hbm", "kernel": "sha_mma_kernel", "achieved": achieved, "peak": hbm_peak,
                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-                         "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, same workload)"
-                         if traffic is not None else None,
-                         "peak_kind": peak_kind, "bytes_per_launch": sha_bytes, "us_per_launch": sha_ms * 1e3},
-            "kernels": {"sparse_mlp_us_per_layer": None if mlp_ms is None else mlp_ms * 1e3,
-                        "sparse_mlp_GBps": None if mlp_ms is None else mlp_bytes / (mlp_ms * 1e-3) / 1e9},
+                         "traffic_source": traffic_src, "peak_kind": peak_kind, "bytes_per_launch": sha_bytes,
+                         "us_per_launch": sha_ms * 1e3},
+            "kernels": mlp,
+            "configs": extra,
             "cpu_baseline": cpu,
             "clocks": clocks,
         }

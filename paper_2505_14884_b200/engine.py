@@ -408,9 +408,9 @@ class DecodeEngine:
                              residual=self.x, expected=self.union_est[ell])
                     n += 2
                 else:
-                    n += self.tp.mlp(self, lw, self.union_idx, cnt)
+                    n += self.tp.mlp(self, lw, self.union_idx, cnt, ell)
             elif self.tp is not None:
-                n += self.tp.mlp(self, lw, None, None)
+                n += self.tp.mlp(self, lw, None, None, ell)
             elif cfg.activation == "swiglu":
                 mk = lw.mlp
                 if self.dense_backend == "cublas":

@@ -183,45 +183,55 @@ class TensorParallel:
         if self.plan.world > 1:
             import torch.distributed as dist
 
+            if t.dtype == torch.bfloat16 and dist.get_backend(self.group) == "gloo":
+                f = t.float()  # CPU-test transport (gloo): no bf16 reduction
+                dist.all_reduce(f, op=dist.ReduceOp.SUM, group=self.group)
+                t.copy_(f)
+                return
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
     def _partial(self, eng, name):
+        """bf16 (B, d) buffer for a rank's partial residual update: the
+        all-reduce moves half the bytes of f32 partials (SURVEY.md §8(e)
+        budgets bf16); the sum is added into the f32 residual stream."""
         t = self._tmp.get(name)
         if t is None:
-            t = torch.zeros_like(eng.x)
+            t = torch.zeros(eng.x.shape, dtype=torch.bfloat16, device=eng.x.device)
             self._tmp[name] = t
         return t
 
     def o_proj(self, eng, lw) -> int:
         """x += all_reduce(attn_local @ W_o[local rows] (+ b_o on rank 0))."""
         part = self._partial(eng, "o")
-        n = eng._linear_f32(eng.attn, lw.w_o_t, lw.b_o, part, residual=False, tag="gg_o")
+        n = eng._linear_bf16(eng.attn, lw.w_o_t, lw.b_o, part, tag="gg_o")
         self.all_reduce(part)
         eng.x.add_(part)
         return n
 
-    def mlp(self, eng, lw, idx, cnt) -> int:
+    def mlp(self, eng, lw, idx, cnt, ell: int = 0) -> int:
         """x += all_reduce(MLP over this rank's neurons (+ b2 on rank 0))."""
         part = self._partial(eng, "mlp")
         mk = lw.mlp
         n = 0
         if idx is not None:
-            mlp_into(mk, eng.h, idx, cnt, eng.hidden, part, residual=None)
+            mlp_into(mk, eng.h, idx, cnt, eng.hidden, part, residual=None, expected=eng.union_est[ell])
             n += 2
         elif eng.cfg.activation == "swiglu":
             torch.mm(eng.h, mk.gate_up().t(), out=eng.gu)
             _lib.call("ps_swiglu", _lib.ptr(eng.gu), eng.gu.stride(0), eng.B, mk.D, _lib.ptr(eng.hidden),
                       eng.hidden.stride(0), _lib.stream_ptr())
-            torch.mm(eng.hidden[:, :mk.D], mk.w2t, out_dtype=torch.float32, out=part)
-            if mk.b2 is not None:
-                part.add_(mk.b2)
             n += 1
+            if mk.b2 is not None:
+                torch.addmm(eng._bf(mk.b2), eng.hidden[:, :mk.D], mk.w2t, out=part)
+            else:
+                torch.mm(eng.hidden[:, :mk.D], mk.w2t, out=part)
         else:
             hid = eng._scratch("hid_tp", (eng.B, mk.D), torch.bfloat16)
             n += eng._linear_bf16(eng.h, mk.w1t, mk.b1, hid, act_relu=True)
-            torch.mm(hid, mk.w2t, out_dtype=torch.float32, out=part)
             if mk.b2 is not None:
-                part.add_(mk.b2)
+                torch.addmm(eng._bf(mk.b2), hid, mk.w2t, out=part)
+            else:
+                torch.mm(hid, mk.w2t, out=part)
         self.all_reduce(part)
         eng.x.add_(part)
         return n

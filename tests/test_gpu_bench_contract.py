@@ -39,6 +39,18 @@ def test_bench_line_has_the_contract_keys():
     assert r["bound"] == "hbm" and r["achieved"] > 0 and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-6
     assert j["cpu_baseline"]["kind"] in ("port", "reference") and j["cpu_baseline"]["cores"] >= 1
     assert "workload" in j["config"]
+    # GPU-only facts stay out of `config` (the reference arm prints the same config)
+    for k in ("kv_storage_buffers", "graph_captured", "kv_aliasing"):
+        assert k not in j["config"] and k in j["setup"]
+    assert j["setup"]["graph_captured"] is True
+    # e2e runs through DecodeEngine.step() and cannot beat the device-timed replay
+    assert j["e2e"]["value"] <= j["value"] * 1.02
+    assert j["union_density_measured"] is not None and 0 < j["union_density_measured"] <= 1
+    assert j["kernels"]["union_size"] >= 1
+    ref = _run("--impl", "reference", "--config", "tiny", "--batch", "8", "--ctx", "200", "--steps", "1",
+               "--warmup", "1", "--cpu-batch", "2")
+    assert ref["config"] == j["config"]
+    assert ref["metric"] == j["metric"] and ref["unit"] == j["unit"]
 
 
 def test_reference_arm_line():
