@@ -10,9 +10,9 @@ N(0, 0.02), synthetic N(0,1) KV history of ``ctx`` tokens, batch 64, head
 density rho = 0.5 (16 of 32 heads from the head router's top-k; layer 0
 dense).  Neuron selection follows the reference's heavy-tailed
 "hot-neuron" recipe (analysis.py:124-140): every token keeps its top
-k = 0.1*D router logits; a fixed hot set (sized so that the batch union
-|S| is ~``--union``*D at B = 64) fires on every token, the remaining picks
-vary token by token, so |S| grows with the batch as in the paper.  A "step"
+k = 0.1*D router logits; a fixed hot set (7.2 % of D: the batch union is
+~0.5*D at B = 64) fires on every token, the remaining picks vary token by
+token, so |S| grows with the batch as in the paper.  A "step"
 = one full decode step (embed -> L x [LN, QKV, KV append, head router +
 top-k, SHA, O-proj, LN, MLP router, top-k, union, selective MLP] -> LN ->
 LM head -> argmax), replayed from one CUDA graph.  Inputs exceed L2
@@ -71,7 +71,9 @@ def parse(argv=None):
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--ctx", type=int, default=1920)
     ap.add_argument("--rho", type=float, default=0.5)
-    ap.add_argument("--union", type=float, default=0.5, help="target |S|/D of the MLP union at batch 64")
+    ap.add_argument("--union", type=float, default=0.5, help="hot-set recipe: |S|/D (= k/D)")
+    ap.add_argument("--hot-frac", type=float, default=0.072,
+                    help="hot-cold recipe: hot-set size / D (0.072: |S|/D ~ 0.5 at B=64, OPT-6.7B)")
     ap.add_argument("--k-frac", type=float, default=0.1, help="per-token neuron budget k / D")
     ap.add_argument("--union-recipe", default="hot-cold", choices=["hot-cold", "hot-set"],
                     help="hot-cold: per-token top-k over a fixed hot set + varying cold picks (default); "
@@ -172,41 +174,24 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workload recipe
-def hot_cold_hot_set(D: int, k: int, target: float, batch: int = 64) -> int:
-    """Hot-set size of the heavy-tailed neuron recipe (analysis.py:124-140).
-
-    Every token keeps its top k neurons: the n_hot hot ones (a large router
-    bias: they fire on every token, hot_p ~ 1) plus k - n_hot cold picks
-    that vary token by token.  With independent cold picks the expected
-    union over ``batch`` tokens is n_hot + C*(1 - exp(-batch*(k - n_hot)/C)),
-    C = D - n_hot; solve it for |S| = target*D by bisection (the measured
-    union is reported next to every number).
-    """
-    want = target * D
-
-    def union(n):
-        c, C = k - n, D - n
-        return n + C * (1.0 - math.exp(-batch * c / C)) if C > 0 else D
-
-    if union(0) <= want:
-        return 0
-    lo, hi = 0, k
-    while hi - lo > 1:
-        mid = (lo + hi) // 2
-        if union(mid) > want:
-            lo = mid
-        else:
-            hi = mid
-    return hi
-
-
 def neuron_recipe(args, D: int):
-    """(k per token, hot-set size) of the MLP selection."""
+    """(k per token, hot-set size) of the MLP selection.
+
+    hot-cold (default; the reference's heavy-tailed profile,
+    analysis.py:124-140): every token keeps its top k = k_frac*D router
+    logits.  A hot set of hot_frac*D neurons carries a large router bias, so
+    it fires on every token (hot_p ~ 1); the remaining picks come from the
+    centered random router and vary token by token, so the batch union |S|
+    grows with the batch.  hot_frac = 0.072 gives |S|/D ~ 0.5 at B = 64 on the
+    OPT-6.7B shape (measured on B200 with tools/union_calib.py: 1000 hot ->
+    0.60, 1500 -> 0.32); the measured |S| is reported next to every number.
+    hot-set: every token's top-k is exactly the hot set (k = |S| = union*D).
+    """
     if args.union_recipe == "hot-set":
         k = max(1, int(round(args.union * D)))
         return k, k
     k = max(1, int(round(args.k_frac * D)))
-    return k, hot_cold_hot_set(D, k, args.union)
+    return k, min(k, int(round(args.hot_frac * D)))
 
 
 def workload_config(args, cfg, batch=None, config=None, ctx=None, world=1, tp=False):
@@ -218,8 +203,9 @@ def workload_config(args, cfg, batch=None, config=None, ctx=None, world=1, tp=Fa
     k, n_hot = neuron_recipe(args, D)
     return {"workload": f"{config} polar decode step", "model_shape": config, "global_batch": batch,
             "seq_len": ctx, "head_density": args.rho,
-            "neuron_selection": (f"per-token top-{k} (k/D={k / D:.3f}) over a hot set of {n_hot} + per-token "
-                                 f"cold picks (analysis.py:124-140); target |S|/D={args.union} at B=64")
+            "neuron_selection": (f"per-token top-{k} (k/D={k / D:.3f}): a hot set of {n_hot} on every token + "
+                                 f"per-token picks of a centered random router (analysis.py:124-140 profile)"
+                                 if args.union_recipe == "hot-cold" else f"every token's top-{k} = one hot set")
             if cfg.activation == "relu" else "dense SwiGLU MLP (never sparsified, engine.py:67-70)",
             "layers": cfg.layers, "d_model": cfg.model_dim, "ffn": cfg.ffn_dim, "heads": cfg.heads,
             "kv_heads": cfg.kv_heads, "parallelism": (f"tp{world}" if tp else f"dp{world}"),
@@ -446,7 +432,8 @@ class Setup:
         mr = None
         if self.relu:
             mr = [pb.MlpRouter.random_device(cfg.model_dim, D, seed=200 + ell, device=dev,
-                                             hot=gen.choice(D, n_hot, replace=False) if n_hot else None)
+                                             hot=gen.choice(D, n_hot, replace=False) if n_hot else None,
+                                             center=args.union_recipe == "hot-cold")
                   for ell in range(L)]
         polar = SparsityPolicy(mode="polar", head_density=args.rho,
                                mlp_k_table={ell: k for ell in range(L)} if self.relu else None)

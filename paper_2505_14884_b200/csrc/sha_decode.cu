@@ -133,7 +133,7 @@ struct PageCursor {
 
 template <int D_H, int G>
 constexpr size_t sha_smem_bytes() {
-  return 2 * kStages * kTileBytes + 64 + (size_t)kWarps * G * (D_H + 2) * 4 + 32;  // flag + kWarps length partials
+  return 2 * kStages * kTileBytes + 64 + (size_t)kWarps * G * (D_H + 2) * 4 + 32;  // flag, kWarps length partials, tile count
 }
 
 template <bool BF16>
@@ -160,6 +160,14 @@ PS_DEV void sha_len_partial(const ShaParams& p, int* scratch) {
   for (int b = threadIdx.x; b < p.B; b += kThreads) m = max(m, __ldg(p.lengths + b));
   m = __reduce_max_sync(0xffffffffu, m);
   if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = m;
+}
+// the tile count lives in shared memory (flag[5]) and is re-read where it is
+// used: keeping it in a register across the main loop pushed the tensor-core
+// kernel past 168 registers (3 CTAs / SM -> 2) and cost ~9 % of the stream rate
+PS_DEV int ld_nt(const int* s) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(s)));
+  return v;
 }
 PS_DEV int sha_nt(const ShaParams& p, const int* scratch, int T) {
   int m = scratch[0];
@@ -215,30 +223,24 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   // first unit's selection / length under the host's tile-count hint: loaded
   // before the barrier setup so the latency overlaps it (every thread needs
   // them for its first segment); reloaded if the device tile count differs
-  int NT = p.NT_hint;
-  long long F = (long long)n_units * NT;
-  long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
-  int u_first = f1 > f0 ? (int)(f0 / NT) : 0;
-  int sel_first = __ldg(p.sel + u_first);
-  int len_first = __ldg(p.lengths + u_first / p.top_k);
+  // first unit = floor(units * bid / n_ctas) whatever the tile count
+  // (floor(floor(U*NT*bid/n) / NT) = floor(U*bid/n)), so its selection and
+  // length load before the tile count is known
+  const int u_first = min(n_units - 1, (int)((long long)n_units * bid / p.n_ctas));
+  const int sel_first = __ldg(p.sel + u_first);
+  const int len_first = __ldg(p.lengths + u_first / p.top_k);
   sha_len_partial(p, flag + 1);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  NT = sha_nt(p, flag + 1, S::T);
-  if (NT != p.NT_hint) {
-    F = (long long)n_units * NT;
-    f0 = (long long)bid * F / p.n_ctas;
-    f1 = (long long)(bid + 1) * F / p.n_ctas;
-    const int u = f1 > f0 ? (int)(f0 / NT) : 0;
-    if (u != u_first) {
-      u_first = u;
-      sel_first = __ldg(p.sel + u_first);
-      len_first = __ldg(p.lengths + u_first / p.top_k);
-    }
+  {
+    const int nt = sha_nt(p, flag + 1, S::T);
+    flag[5] = nt;  // every thread stores the same value
   }
+  const long long f0 = (long long)bid * ((long long)n_units * ld_nt(flag + 5)) / p.n_ctas;
+  const long long f1 = (long long)(bid + 1) * ((long long)n_units * ld_nt(flag + 5)) / p.n_ctas;
   const int n_it = (int)(f1 - f0);
 
   // producer (thread 0): walks the flattened tiles in order with an
@@ -271,12 +273,13 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
       bulk_g2s(sK + stage * S::T * D_H, p.k + off, bytes, &bars[stage]);
       bulk_g2s(sV + stage * S::T * D_H, p.v + off, bytes, &bars[stage]);
     }
-    if (++cur.t == NT) {  // advance the cursor
+    if (++cur.t == ld_nt(flag + 5)) {  // advance the cursor
       cur.t = 0;
       if (cur.u + 1 < n_units) load_unit(cur.u + 1);
     }
   };
   if (tid == 0 && n_it > 0) {
+    const int NT = ld_nt(flag + 5);
     const int u0 = (int)(f0 / NT);
     cur.t = (int)(f0 - (long long)u0 * NT);
     load_unit(u0);
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
   int it = 0;
   long long f = f0;
   while (f < f1) {
+    const int NT = ld_nt(flag + 5);
     const int u = (int)(f / NT);
     const long long u_end = (long long)(u + 1) * NT;
     const long long seg_end = f1 < u_end ? f1 : u_end;
@@ -428,7 +432,8 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
     __syncthreads();
 
     // ---- merge warps; a unit inside one CTA writes its output directly
-    const int c_first = cta_of((long long)u * NT, F, p.n_ctas);
+    const long long F = (long long)n_units * ld_nt(flag + 5);
+    const int c_first = cta_of((long long)u * ld_nt(flag + 5), F, p.n_ctas);
     const int c_last = cta_of(u_end - 1, F, p.n_ctas);
     const int nseg = c_last - c_first + 1, seg = bid - c_first;
     const size_t out_row = (size_t)b * p.out_ld + (size_t)g * G * D_H;
@@ -537,7 +542,7 @@ PS_DEV uint32_t mma_sw(int r, int C) {
 }
 
 template <int G, bool OUT_BF16>
-__global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant__ CUtensorMap tmK,
+__global__ void __launch_bounds__(kThreads, 3) sha_mma_kernel(const __grid_constant__ CUtensorMap tmK,
                                                           const __grid_constant__ CUtensorMap tmV, const ShaParams p) {
   constexpr int D_H = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -580,12 +585,12 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
   }
 
   // tile count from the device lengths (see ShaParams::NT_hint)
-  int NT = p.NT_hint;
-  long long F = (long long)n_units * NT;
-  long long f0 = (long long)bid * F / p.n_ctas, f1 = (long long)(bid + 1) * F / p.n_ctas;
-  int u_first = f1 > f0 ? (int)(f0 / NT) : 0;
-  int sel_first = __ldg(p.sel + u_first);
-  int len_first = __ldg(p.lengths + u_first / p.top_k);
+  // first unit = floor(units * bid / n_ctas) whatever the tile count
+  // (floor(floor(U*NT*bid/n) / NT) = floor(U*bid/n)), so its selection and
+  // length load before the tile count is known
+  const int u_first = min(n_units - 1, (int)((long long)n_units * bid / p.n_ctas));
+  const int sel_first = __ldg(p.sel + u_first);
+  const int len_first = __ldg(p.lengths + u_first / p.top_k);
   sha_len_partial(p, flag + 1);
   if (tid == 0) {
     prefetch_tmap(&tmK);
@@ -594,18 +599,12 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
     fence_mbar_init();
   }
   __syncthreads();
-  NT = sha_nt(p, flag + 1, kMmaT);
-  if (NT != p.NT_hint) {
-    F = (long long)n_units * NT;
-    f0 = (long long)bid * F / p.n_ctas;
-    f1 = (long long)(bid + 1) * F / p.n_ctas;
-    const int u = f1 > f0 ? (int)(f0 / NT) : 0;
-    if (u != u_first) {
-      u_first = u;
-      sel_first = __ldg(p.sel + u_first);
-      len_first = __ldg(p.lengths + u_first / p.top_k);
-    }
+  {
+    const int nt = sha_nt(p, flag + 1, kMmaT);
+    flag[5] = nt;  // every thread stores the same value
   }
+  const long long f0 = (long long)bid * ((long long)n_units * ld_nt(flag + 5)) / p.n_ctas;
+  const long long f1 = (long long)(bid + 1) * ((long long)n_units * ld_nt(flag + 5)) / p.n_ctas;
   const int n_it = (int)(f1 - f0);
 
   // producer cursor (thread 0)
@@ -637,13 +636,13 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
       tma_load_2d(v_dst, &tmV, 0, row, &bars[stage]);
       tma_load_2d(v_dst + 4096, &tmV, 64, row, &bars[stage]);
     }
-    if (++cur.t == NT) {
+    if (++cur.t == ld_nt(flag + 5)) {
       cur.t = 0;
       if (cur.u + 1 < n_units) load_unit(cur.u + 1);
     }
   };
   if (tid == 0 && n_it > 0) {
-    cur.t = (int)(f0 - (long long)u_first * NT);
+    cur.t = (int)(f0 - (long long)u_first * ld_nt(flag + 5));
     load_unit(u_first);
     const int pre = min(kMmaStages, n_it);
     for (int s2 = 0; s2 < pre; ++s2) issue_next(s2);
@@ -657,6 +656,7 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
   int it = 0;
   long long f = f0;
   while (f < f1) {
+    const int NT = ld_nt(flag + 5);
     const int u = (int)(f / NT);
     const long long u_end = (long long)(u + 1) * NT;
     const long long seg_end = f1 < u_end ? f1 : u_end;
@@ -769,7 +769,8 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
     __syncthreads();
 
     // ---- merge warps; a unit inside one CTA writes its output directly
-    const int c_first = cta_of((long long)u * NT, F, p.n_ctas);
+    const long long F = (long long)n_units * ld_nt(flag + 5);
+    const int c_first = cta_of((long long)u * ld_nt(flag + 5), F, p.n_ctas);
     const int c_last = cta_of(u_end - 1, F, p.n_ctas);
     const int nseg = c_last - c_first + 1, seg = bid - c_first;
     const size_t out_row = (size_t)b * p.out_ld + (size_t)g * G * D_H;
@@ -832,7 +833,7 @@ __global__ void __launch_bounds__(kThreads) sha_mma_kernel(const __grid_constant
 
 template <int G>
 constexpr size_t sha_mma_smem_bytes() {
-  return 1024 + 2 * kMmaStages * kMmaTileBytes + 64 + (size_t)kWarps * G * (128 + 2) * 4 + 32;  // flag + kWarps length partials
+  return 1024 + 2 * kMmaStages * kMmaTileBytes + 64 + (size_t)kWarps * G * (128 + 2) * 4 + 32;  // flag, kWarps length partials, tile count
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_sha_encode = nullptr;

@@ -211,6 +211,17 @@ class DecodeEngine:
         self.graph = None
         self.launches_per_step = None
         self.record = None  # eager-only debug capture of selections (parity tests)
+        self.trace = None   # device copies of every layer's selections, captured with the graph (tests)
+
+    def enable_trace(self) -> None:
+        """Keep a device copy of every layer's head selection and neuron union
+        (two D2D copies per layer, recorded into the captured graph too), so a
+        replayed step's own selections can be read back: ``trace["heads"][l]``
+        (B, k_h), ``trace["union"][l][:union_counts[l]]``.  Call before
+        ``capture()``; for parity tests, not for timing."""
+        L, dev = self.cfg.layers, self.device
+        self.trace = {"heads": [torch.zeros(self.B, max(1, k), dtype=torch.int32, device=dev) for k in self.k_heads],
+                      "union": [torch.zeros_like(self.union_idx) if self.sparse_mlp else None for _ in range(L)]}
 
     # ------------------------------------------------------------------ state
     @property
@@ -361,6 +372,8 @@ class DecodeEngine:
                 n += 1
             else:
                 sel = self.sel_full
+            if self.trace is not None and k_h:
+                self.trace["heads"][ell].copy_(sel)
             # the hint only sizes the grid: the kernel reads the tile count from
             # the device lengths, so a captured graph stays exact as they grow
             sha_decode_into(self.qkv, qkv_w, c, sel, self.H_loc, self.scale, self.attn, self.d_loc,
@@ -396,6 +409,8 @@ class DecodeEngine:
                                              lo, hi, ROW_PAD, _lib.ptr(self.union_idx),
                                              _lib.ptr(cnt), st), "ps_select_union")
                 n += 1
+                if self.trace is not None:
+                    self.trace["union"][ell].copy_(self.union_idx)
                 if self.record is not None:
                     lg = self.r_logits.clone()
                     if out_bias is not None:

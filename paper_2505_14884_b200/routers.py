@@ -137,7 +137,7 @@ class MlpRouter:
 
     @classmethod
     def random_device(cls, d_model: int, ffn_dim: int, hidden_dim: int | None = None, seed: int = 0,
-                      device=None, hot=None, hot_bias: float = 20.0) -> "MlpRouter":
+                      device=None, hot=None, hot_bias: float = 20.0, center: bool = False) -> "MlpRouter":
         """Router drawn on the device with the reference's distribution
         (N(0, sqrt(2/d)), N(0, sqrt(2/h)), zero biases) -- for production
         shapes where host-side init is slow.  ``hot`` (neuron ids) adds
@@ -155,6 +155,13 @@ class MlpRouter:
         obj.w_out_t = (torch.randn(ffn_dim, h, device=dev, generator=gen) * math.sqrt(2.0 / h)).to(torch.bfloat16)
         obj.b_in = torch.zeros(h, device=dev)
         obj.b_out = torch.zeros(ffn_dim, device=dev)
+        if center:
+            # remove the token-independent part of the logits: for unit-variance
+            # inputs the hidden pre-activations are N(0, 2), so E[relu] = 1/sqrt(pi)
+            # and every logit carries the constant offset E[relu] * sum_i W_out[i, j];
+            # subtracting it leaves per-token (not per-neuron) variation, so the
+            # non-hot picks differ from token to token
+            obj.b_out -= obj.w_out_t.float().sum(dim=1) / math.sqrt(math.pi)
         if hot is not None:
             obj.b_out[torch.as_tensor(np.asarray(hot), device=dev, dtype=torch.long)] += hot_bias
         return obj
