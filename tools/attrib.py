@@ -69,12 +69,16 @@ def main():
     ap.add_argument("--ctx", type=int, default=1920)
     ap.add_argument("--rho", type=float, default=0.5)
     ap.add_argument("--union", type=float, default=0.5)
+    ap.add_argument("--k-frac", type=float, default=0.1)
+    ap.add_argument("--hot-frac", type=float, default=0.072)
+    ap.add_argument("--union-recipe", default="hot-cold")
     ap.add_argument("--mode", default="polar")
     a = ap.parse_args()
+    import bench  # the bench's neuron recipe (hot/cold, centered router)
     dev = torch.device("cuda", 0)
     cfg = SHAPES[a.config]
     L, H_kv, D = cfg.layers, cfg.kv_heads, cfg.ffn_dim
-    k_mlp = max(1, int(round(a.union * D)))
+    k_mlp, n_hot = bench.neuron_recipe(a, D)
     gen = np.random.default_rng(7)
     model = DeviceModel.random(cfg, seed=1234, device=dev)
     relu = cfg.activation == "relu"
@@ -82,7 +86,8 @@ def main():
     mr = None
     if relu:
         mr = [pb.MlpRouter.random_device(cfg.model_dim, D, seed=200 + e, device=dev,
-                                         hot=gen.choice(D, k_mlp, replace=False)) for e in range(L)]
+                                         hot=gen.choice(D, n_hot, replace=False) if n_hot else None,
+                                         center=a.union_recipe == "hot-cold") for e in range(L)]
     if a.mode == "polar":
         pol = SparsityPolicy(mode="polar", head_density=a.rho,
                              mlp_k_table={e: k_mlp for e in range(L)} if relu else None)
@@ -92,6 +97,7 @@ def main():
     eng.fill_random(a.ctx, seed=99)
     eng.tokens.copy_(torch.randint(0, cfg.vocab, (a.batch,), dtype=torch.int32))
     lens = [c.lengths.clone() for c in eng.caches]
+
 
     orig = {"sha": E.sha_decode_into, "mlp": E.mlp_into, "lib": _lib.load, "torch": E.torch,
             "lb": eng._linear_bf16, "lf": eng._linear_f32, "ln": eng._ln, "hs": eng._head_select}
