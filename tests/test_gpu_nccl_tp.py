@@ -1,9 +1,9 @@
 """TP=2 over NCCL on two GPUs (runs only when >= 2 CUDA devices are visible;
 the driver's GPU box has one, so this is skipped there and runs on a
 multi-GPU host).  Each rank decodes its shard (heads + neurons) with bf16
-partials all-reduced by NCCL inside the captured graph; rank 0 compares the
-logits with the TP=1 engine on the same model and inputs, eager and from
-graph replays."""
+partials all-reduced by NCCL, eagerly and then from a captured graph; rank 0
+compares every step's logits with the oracle decode step forced to the
+engine's own (traced) global selections, the steps replayed in order."""
 
 import os
 import socket
@@ -29,7 +29,7 @@ def _port():
 def _rank(rank, world, port, kv_heads, mode, q):
     import torch.distributed as dist
 
-    from test_gpu_tp import _build
+    from test_gpu_tp import CFG, _build, oracle_logits, selections_from_trace
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -38,18 +38,23 @@ def _rank(rank, world, port, kv_heads, mode, q):
         from paper_2505_14884_b200.model import TransformerConfig
         from paper_2505_14884_b200.parallel import TPPlan, TensorParallel
 
-        cfg = TransformerConfig(2, 256, 1024, 8, kv_heads, 512, 288, "relu")
+        L, d, D, H, V, S = CFG
+        cfg = TransformerConfig(L, d, D, H, kv_heads, V, S, "relu")
         plan = TPPlan.make(cfg, world, rank)
         eng, tokens = _build(kv_heads, mode, tp=TensorParallel(plan), plan=plan)
+        eng.enable_trace()
+        steps = []
         outs = [eng.step(tokens).cpu().numpy()]
+        steps.append(selections_from_trace(eng, plan, world))
         eng.capture()
         for _ in range(3):
             outs.append(eng.step(tokens).cpu().numpy())
+            steps.append(selections_from_trace(eng, plan, world))
         if rank == 0:
-            ref_eng, _ = _build(kv_heads, mode)
             errs = []
-            for o in outs:
-                ref = ref_eng.step(tokens).cpu().numpy()
+            for i, o in enumerate(outs):
+                before = [(tokens, h, u) for h, u in steps[:i]]
+                ref = oracle_logits(kv_heads, mode, tokens, steps[i][0], steps[i][1], steps_before=before)
                 errs.append(float(np.linalg.norm(o - ref) / np.linalg.norm(ref)))
             q.put(errs)
     finally:
@@ -57,7 +62,7 @@ def _rank(rank, world, port, kv_heads, mode, q):
 
 
 @pytest.mark.parametrize("kv_heads,mode", [(8, "polar"), (2, "polar"), (8, "dense")])
-def test_tp2_nccl_matches_tp1(kv_heads, mode):
+def test_tp2_nccl_matches_oracle(kv_heads, mode):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
