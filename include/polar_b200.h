@@ -249,6 +249,39 @@ int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t* idx, const
                      void* out, int64_t out_ld, int out_dtype,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* ps_sparse_mlp -- the whole selective MLP in ONE launch (replaces
+ * sparse_mlp_forward, kernels.py:353-373, and the engine's per-layer MLP
+ * block, engine.py:371-392):
+ *   hidden[n, j] = relu( sum_k w1_rows[idx[j], k] x[n, k] + b1[idx[j]] )  (bf16, j < count;
+ *                  columns [count, round_up(count, 128)) written as 0)
+ *   out[n, m]   += sum_{j < count} hidden[n, j] w2_rows[idx[j], m] + b2[m]   (f32, ACCUMULATED:
+ *                  out holds the residual stream, or zeros, on entry)
+ *   count = *count_dev (idx == count_dev == NULL: every neuron, the dense MLP).
+ *   w1_rows / w2_rows: bf16 (D, d) neuron-major (W1^T, W2^T); x bf16 (N, d); hidden bf16 (N, h_ld >= round_up(D,128));
+ *   N <= 256.  One persistent CTA per SM, stream-K over both projections:
+ *   split up-projection tiles are summed with f32 reductions and finished by
+ *   their last piece; each down-projection K block waits only on the
+ *   up-projection tile it reads (device flags) and adds its partial into out.
+ *   No second launch, no grid barrier.  The f32 reductions make the last bits
+ *   of out depend on arrival order (results agree to f32 rounding).
+ *   ws: zero-initialised once, ps_sparse_mlp_workspace_bytes(N, D, d) bytes,
+ *   self-resetting (CUDA-graph safe); one stream at a time per workspace. */
+size_t ps_sparse_mlp_workspace_bytes(int N, int D, int d);
+int ps_sparse_mlp(const void* w1_rows, const float* b1, const void* w2_rows, const float* b2, int D, int d,
+                  const int32_t* idx, const int32_t* count_dev, const void* x, int64_t x_ld, int N,
+                  void* hidden, int64_t h_ld, float* out, int64_t out_ld, void* ws, size_t ws_bytes, void* stream);
+
+/* ps_router_mlp -- the two-layer neuron router in ONE launch (replaces
+ * MlpRouter.decision_function, routers.py:286-288):
+ *   hid = relu(x W_in + b_in) (bf16 (N, hid_ld)), logits = hid W_out + b_out (f32; b_out may be NULL,
+ *   e.g. when ps_select_union adds it).  w_in_rows = W_in^T (h, d), w_out_rows = W_out^T (D, h), bf16. */
+size_t ps_router_mlp_workspace_bytes(int N, int h, int D);
+int ps_router_mlp(const void* w_in_rows, const float* b_in, const void* w_out_rows, const float* b_out,
+                  int d, int h, int D, const void* x, int64_t x_ld, int N, void* hid, int64_t hid_ld,
+                  float* logits, int64_t logits_ld, void* ws, size_t ws_bytes, void* stream);
+void ps_debug_chain_stages(int stages);
+void ps_debug_chain_trace(void* buf);
+
 /* ======================================================================
  * Decode-step glue.
  * ps_layernorm: model.layernorm (model.py:168-175): x f32 (B, d) row b at

@@ -62,6 +62,13 @@ SIGNATURES = {
                             _vp, _i64, _i, _vp, _sz, _vp]),
     "ps_gather_gemm_t": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i,
                               _vp, _i64, _i, _vp, _sz, _vp]),
+    "ps_sparse_mlp_workspace_bytes": (_sz, [_i, _i, _i]),
+    "ps_sparse_mlp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _sz,
+                           _vp]),
+    "ps_router_mlp_workspace_bytes": (_sz, [_i, _i, _i]),
+    "ps_router_mlp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _sz, _vp]),
+    "ps_debug_chain_stages": (None, [_i]),
+    "ps_debug_chain_trace": (None, [_vp]),
     "ps_set_pdl": (None, [_i]),
     "ps_layernorm": (_i, [_vp, _i64, _vp, _vp, _i, _i, _vp, _i64, _vp]),
     "ps_add_layernorm": (_i, [_vp, _i64, _vp, _vp, _vp, _i, _i, _vp, _i64, _vp]),

@@ -27,7 +27,7 @@ import torch
 
 from . import _lib, _ws
 from .exceptions import CapacityError, ConfigurationError
-from .kernels import ROW_PAD, _round_up, gather_gemm_into, mlp_into, sha_decode_into, swiglu_into
+from .kernels import ROW_PAD, _round_up, gather_gemm_into, mlp_into, sha_decode_into, sparse_mlp_into, swiglu_into
 from .model import DeviceModel, TransformerConfig
 from .tensors import KVCache, PagedKVCache
 from .validation import check_choice, check_count
@@ -88,7 +88,8 @@ class DecodeEngine:
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
                  caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
-                 concurrent_router: bool = False, kv_page_rows: int = 0, kv_reserve: str = "full"):
+                 concurrent_router: bool = False, kv_page_rows: int = 0, kv_reserve: str = "full",
+                 mlp_backend: str = "split"):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
@@ -101,6 +102,10 @@ class DecodeEngine:
         # head router on a side stream, concurrent with the QKV GEMM (a
         # parallel branch of the captured graph); False = fused with the append
         self.concurrent_router = concurrent_router
+        # selective MLP: "split" = UP and DOWN as two tcgen05 launches
+        # (ps_gather_gemm / _t); "chain" = both in one persistent launch
+        # (ps_sparse_mlp, batch <= 256)
+        self.mlp_backend = check_choice(mlp_backend, ("split", "chain"), "mlp_backend")
         self.side = torch.cuda.Stream(device=model.device) if concurrent_router else None
         self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
@@ -418,7 +423,10 @@ class DecodeEngine:
                     self.record.setdefault("mlp_logits", []).append(lg)
                     self.record.setdefault("union", []).append(
                         self.union_idx[: int(cnt.item())].clone())
-                if self.tp is None:
+                if self.tp is None and self.mlp_backend == "chain" and B <= 256:
+                    sparse_mlp_into(lw.mlp, self.h, self.union_idx, cnt, self.hidden, self.x, residual=self.x)
+                    n += 1
+                elif self.tp is None:
                     mlp_into(lw.mlp, self.h, self.union_idx, cnt, self.hidden, self.x,
                              residual=self.x, expected=self.union_est[ell])
                     n += 2

@@ -435,6 +435,27 @@ def mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor,
                        flags=_lib.PS_GG_A_READY)  # idx/count were written before the UP launch
 
 
+def sparse_mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor, out: torch.Tensor,
+                    residual=None, tag: str = "mlp_chain") -> None:
+    """The whole selective MLP in ONE launch (ps_sparse_mlp): UP over the
+    union rows, ReLU, DOWN over the same rows, + b2, ADDED into ``out``
+    (f32).  ``residual``: ``out`` is set to it first (``out`` itself: in
+    place; None: out = MLP only).  ``idx`` / ``count`` None = every neuron.
+    Batch <= 256 (else :func:`mlp_into`)."""
+    B, d = x2d.shape
+    if out.dtype != torch.float32:
+        raise ValueError("sparse_mlp_into accumulates into an f32 output")
+    if residual is None:
+        out.zero_()
+    elif residual is not out:
+        out.copy_(residual)
+    lib = _lib.load()
+    ws = _ws.get(tag, lib.ps_sparse_mlp_workspace_bytes(B, pk.D, d), x2d.device)
+    _lib.call("ps_sparse_mlp", _lib.ptr(pk.w1t), _lib.ptr(pk.b1), _lib.ptr(pk.w2t), _lib.ptr(pk.b2), pk.D, d,
+              _lib.ptr(idx), _lib.ptr(count), _lib.ptr(x2d), x2d.stride(0), B, _lib.ptr(hidden), hidden.stride(0),
+              _lib.ptr(out), out.stride(0), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+
+
 def sparse_mlp_forward(x, w1, b1=None, w2=None, b2=None, active=None) -> torch.Tensor:
     """kernels.py:353-373: ReLU MLP restricted to the union set ``active``.
 

@@ -178,14 +178,27 @@ class MlpRouter:
         return cls(w_in.shape[0], np.asarray(w_out).shape[1], w_in.shape[1], 0, device,
                    _weights=(w_in, b_in, w_out, b_out))
 
-    def logits_into(self, x2d: torch.Tensor, hid: torch.Tensor, logits: torch.Tensor) -> None:
-        """Two tcgen05 launches: hid = relu(x W_in + b_in) (bf16), logits (f32)."""
+    def logits_into(self, x2d: torch.Tensor, hid: torch.Tensor, logits: torch.Tensor, with_bias: bool = True,
+                    fused: bool = False) -> None:
+        """hid = relu(x W_in + b_in) (bf16), logits = hid W_out (+ b_out) (f32).
+        ``fused``: both layers in ONE chained launch (ps_router_mlp; B <= 256;
+        measured slower than the two launches, kept as an option);
+        else two tcgen05 launches (ps_gather_gemm).  ``with_bias=False`` leaves
+        b_out to the consumer (ps_select_union adds it while ranking)."""
         B, d = x2d.shape
         h = self.hidden_dim_
+        if fused and B <= 256:
+            lib = _lib.load()
+            ws = _ws.get("router_chain", lib.ps_router_mlp_workspace_bytes(B, h, self.ffn_dim), x2d.device)
+            _lib.call("ps_router_mlp", _lib.ptr(self.w_in_t), _lib.ptr(self.b_in), _lib.ptr(self.w_out_t),
+                      _lib.ptr(self.b_out) if with_bias else None, d, h, self.ffn_dim, _lib.ptr(x2d),
+                      x2d.stride(0), B, _lib.ptr(hid), hid.stride(0), _lib.ptr(logits), logits.stride(0),
+                      _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+            return
         gather_gemm_into(self.w_in_t, None, None, x2d, x2d.stride(0), self.b_in, B, h, d, _lib.PS_ACT_RELU,
                          hid, hid.stride(0), tag="gg_router")
-        gather_gemm_into(self.w_out_t, None, None, hid, hid.stride(0), self.b_out, B, self.ffn_dim, h,
-                         _lib.PS_ACT_NONE, logits, logits.stride(0), tag="gg_router")
+        gather_gemm_into(self.w_out_t, None, None, hid, hid.stride(0), self.b_out if with_bias else None, B,
+                         self.ffn_dim, h, _lib.PS_ACT_NONE, logits, logits.stride(0), tag="gg_router")
 
     def decision_function(self, x) -> torch.Tensor:
         xb, single = _as_batch(x, self.d_model, self.w_in_t.device)

@@ -73,6 +73,8 @@ def main():
     ap.add_argument("--hot-frac", type=float, default=0.072)
     ap.add_argument("--union-recipe", default="hot-cold")
     ap.add_argument("--mode", default="polar")
+    ap.add_argument("--mlp-backend", default="split")
+    ap.add_argument("--only", default="", help="comma list of components to drop (default: all)")
     a = ap.parse_args()
     import bench  # the bench's neuron recipe (hot/cold, centered router)
     dev = torch.device("cuda", 0)
@@ -93,18 +95,19 @@ def main():
                              mlp_k_table={e: k_mlp for e in range(L)} if relu else None)
     else:
         pol = SparsityPolicy(mode="dense")
-    eng = DecodeEngine(model, a.batch, a.ctx + 16, pol, head_routers=hr, mlp_routers=mr)
+    eng = DecodeEngine(model, a.batch, a.ctx + 16, pol, head_routers=hr, mlp_routers=mr, mlp_backend=a.mlp_backend)
     eng.fill_random(a.ctx, seed=99)
     eng.tokens.copy_(torch.randint(0, cfg.vocab, (a.batch,), dtype=torch.int32))
     lens = [c.lengths.clone() for c in eng.caches]
 
 
-    orig = {"sha": E.sha_decode_into, "mlp": E.mlp_into, "lib": _lib.load, "torch": E.torch,
+    orig = {"sha": E.sha_decode_into, "mlp": E.mlp_into, "smlp": E.sparse_mlp_into, "lib": _lib.load, "torch": E.torch,
             "lb": eng._linear_bf16, "lf": eng._linear_f32, "ln": eng._ln, "hs": eng._head_select}
     lib = _lib.load()
 
     def restore():
         E.sha_decode_into, E.mlp_into, E.torch = orig["sha"], orig["mlp"], orig["torch"]
+        E.sparse_mlp_into = orig["smlp"]
         _lib.load = orig["lib"]
         eng._linear_bf16, eng._linear_f32, eng._ln, eng._head_select = orig["lb"], orig["lf"], orig["ln"], orig["hs"]
 
@@ -113,6 +116,7 @@ def main():
             E.sha_decode_into = lambda *x, **k: None
         elif what == "mlp(up+down)":
             E.mlp_into = lambda *x, **k: None
+            E.sparse_mlp_into = lambda *x, **k: None
         elif what == "select_union":
             _lib.load = lambda: _LibProxy(lib, {"ps_select_union"})
         elif what == "router_gemms":
@@ -133,6 +137,8 @@ def main():
 
     items = ["none", "sha", "mlp(up+down)", "select_union", "router_gemms", "qkv", "o_proj", "layernorm",
              "head_router+append"]
+    if a.only:
+        items = ["none"] + a.only.split(",")
     base = None
     for what in items:
         restore()
