@@ -160,6 +160,9 @@ int ps_select_union(const float* logits, const float* bias, int rows, int cols, 
                     int32_t* union_out, int32_t* count_out, void* stream);
 /* debug: per-CTA phase timestamps of the top-k kernel (16 x u64 per CTA), NULL = off */
 void ps_debug_topk_trace(void* buf);
+/* ps_select_union kernel: 1 = the low-latency row kernel (topk_union.cu,
+ * default for cols <= 36864), 0 = the bracket/candidate kernel (select.cu). */
+void ps_debug_topk_v2(int enable);
 int ps_union_rows(const int32_t* rows_idx, int rows, int k, int width,
                   uint32_t* bitmap, void* stream);
 int ps_bitmap_compact(uint32_t* bitmap, int width, int lo, int hi, int pad,

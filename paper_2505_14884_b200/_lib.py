@@ -56,6 +56,7 @@ SIGNATURES = {
     "ps_debug_gemm_lsu_mode": (None, [_i]),
     "ps_debug_gemm_gemv": (None, [_i]),
     "ps_debug_topk_trace": (None, [_vp]),
+    "ps_debug_topk_v2": (None, [_i]),
     "ps_gather_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "ps_gather_gemm_auto_splits": (_i, [_i, _i, _i]),
     "ps_gather_gemm": (_i, [_vp, _i, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i, _i, _i, _i, _i, _i,

@@ -159,31 +159,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     tr[7] = smid;
   }
 
-  // ---- PDL: with the A operand ready (static weights, or ids produced >= 2
-  // launches earlier) only the B / epilogue roles wait for the previous grid
-  if (!p.a_early) {
-    griddep_wait();
-    if (tid == 0) griddep_launch();
-  }
-  // ---- device-side work partition (identical in every role and CTA of a cluster)
-  const int count = p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K);
-  const int klimit = (MODE == MODE_UP) ? p.K : count;
-  const int kbt = (klimit + BK - 1) / BK;
-  const int live_m = (MODE == MODE_UP) ? (count + BM - 1) / BM : (p.M + BM - 1) / BM;
-  const int tiles = live_m * p.n_tiles;
-  const int per = (kbt + C - 1) / C;
-  const int kb0 = rank * per;
-  const int nkb = max(0, min(kbt, kb0 + per) - kb0);  // K blocks of this CTA (same for every tile)
-  const int my_tiles = cid < tiles ? (tiles - cid + ncl - 1) / ncl : 0;
-  // every CTA of a cluster sees the same my_tiles, so whole clusters leave together
-  if (my_tiles == 0) {
-    if (p.a_early) {
-      griddep_wait();
-      if (tid == 0) griddep_launch();
-    }
-    return;
-  }
-
+  // ---- input-independent prologue first (barrier init, TMEM alloc, tensor
+  // map prefetch): under PDL it overlaps the previous grid's tail
   const uint32_t tcols = NB <= 16 ? 32 : (NB <= 32 ? 64 : (NB <= 64 ? 128 : (NB <= 128 ? 256 : 512)));
   if (warp == kMmaWarp) {
     if (lane == 0) {
@@ -216,6 +193,33 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  // ---- PDL: with the A operand ready (static weights, or ids produced >= 2
+  // launches earlier) only the B / epilogue roles wait for the previous grid
+  if (!p.a_early) {
+    griddep_wait();
+    if (tid == 0) griddep_launch();
+  }
+  // ---- device-side work partition (identical in every role and CTA of a cluster)
+  const int count = p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K);
+  const int klimit = (MODE == MODE_UP) ? p.K : count;
+  const int kbt = (klimit + BK - 1) / BK;
+  const int live_m = (MODE == MODE_UP) ? (count + BM - 1) / BM : (p.M + BM - 1) / BM;
+  const int tiles = live_m * p.n_tiles;
+  const int per = (kbt + C - 1) / C;
+  const int kb0 = rank * per;
+  const int nkb = max(0, min(kbt, kb0 + per) - kb0);  // K blocks of this CTA (same for every tile)
+  const int my_tiles = cid < tiles ? (tiles - cid + ncl - 1) / ncl : 0;
+  // every CTA of a cluster sees the same my_tiles, so whole clusters leave together
+  if (my_tiles == 0) {
+    if (p.a_early) {
+      griddep_wait();
+      if (tid == 0) griddep_launch();
+    }
+    if (warp == kMmaWarp) tmem_dealloc(tmem, tcols);
+    return;
+  }
+
   if (tr && tid == 0) tr[1] = gtimer();
 
   auto tile_of = [&](int j) { return cid + j * ncl; };

@@ -1140,8 +1140,18 @@ extern "C" size_t ps_select_union_workspace_bytes(int rows, int cols) {
   if (rows < 1 || cols < 1) return 0;
   const size_t tickets = (su_groups(rows) + 3 + (size_t)rows) * 4;
   const size_t head = (tickets + 255) / 256 * 256;
-  return head + (su_groups(rows) + (size_t)rows) * su_words(cols) * 4;
+  // + the low-latency kernel's region: a ticket (256 B) and one union bitmap
+  return head + (su_groups(rows) + (size_t)rows) * su_words(cols) * 4 + 256 + su_words(cols) * 4;
 }
+
+namespace ps {
+int select_union_v2(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k, float thr,
+                    int* ticket, uint32_t* bitmap, int lo, int hi, int pad, int32_t* union_out, int32_t* count_out,
+                    unsigned long long* trace, cudaStream_t st);
+int select_union_v2_max_cols();
+}  // namespace ps
+static int g_topk_v2 = -1;  // -1: from env PS_TOPK_V2 (default 1)
+extern "C" void ps_debug_topk_v2(int enable) { g_topk_v2 = enable ? 1 : 0; }
 
 extern "C" int ps_select_union(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k,
                                float thr, void* ws, size_t ws_bytes, int lo, int hi, int pad, int32_t* union_out,
@@ -1151,12 +1161,22 @@ extern "C" int ps_select_union(const float* logits, const float* bias, int rows,
   if (rows > kGroupRows * kMaxGroups) return PS_ERR_UNSUPPORTED;
   if (lo < 0 || lo % 32 || hi > cols || hi <= lo || pad < 1) return PS_ERR_VALUE;
   if (ws_bytes < ps_select_union_workspace_bytes(rows, cols)) return PS_ERR_WORKSPACE;
-  TopkParams prm{};
-  prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k > 0 ? k : 0; prm.thr = thr;
-  prm.bias = bias;
   const size_t tickets = (su_groups(rows) + 3 + (size_t)rows) * 4;
   const size_t head = (tickets + 255) / 256 * 256;
   uint8_t* base = static_cast<uint8_t*>(ws);
+  if (g_topk_v2 < 0) {
+    const char* e = getenv("PS_TOPK_V2");
+    g_topk_v2 = e ? atoi(e) : 1;
+  }
+  if (g_topk_v2 && cols <= select_union_v2_max_cols()) {
+    uint8_t* v2 = base + head + (su_groups(rows) + (size_t)rows) * su_words(cols) * 4;
+    return select_union_v2(logits, bias, rows, cols, ld, k > 0 ? k : 0, thr, reinterpret_cast<int*>(v2),
+                           reinterpret_cast<uint32_t*>(v2 + 256), lo, hi, pad, union_out, count_out, g_topk_trace,
+                           static_cast<cudaStream_t>(stream));
+  }
+  TopkParams prm{};
+  prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k > 0 ? k : 0; prm.thr = thr;
+  prm.bias = bias;
   // one CTA per row and per SM (the kernel's shared memory): all resident
   // at once iff rows <= SMs, and every CTA owns <= 512 words
   prm.coresident = rows <= ps_num_sms() && (cols + 31) / 32 <= (size_t)kUnionWPT * kTopkThreads;
