@@ -285,6 +285,20 @@ int ps_router_mlp(const void* w_in_rows, const float* b_in, const void* w_out_ro
 void ps_debug_chain_stages(int stages);
 void ps_debug_chain_trace(void* buf);
 
+/* ps_router_mlp_fused -- the same router (routers.py:286-288) as one
+ * persistent launch with a device grid barrier between its layers: one CTA
+ * per 128 logit columns (D <= 128 * #SMs, all co-resident), W_in split over
+ * the CTAs (<= 4 K-blocks each), both layers' static weights TMA-prefetched
+ * before the dependency wait.  N <= 128, d % 64 == 0, h % 128 == 0; other
+ * shapes return PS_ERR_UNSUPPORTED (callers fall back to ps_router_mlp or two
+ * GEMMs).  ws: ps_router_mlp_fused_workspace_bytes(N, d, h, D) bytes,
+ * zero-initialised once (self-resetting barrier word + f32 partials). */
+size_t ps_router_mlp_fused_workspace_bytes(int N, int d, int h, int D);
+int ps_router_mlp_fused(const void* w_in_rows, const float* b_in, const void* w_out_rows, const float* b_out,
+                        int d, int h, int D, const void* x, int64_t x_ld, int N, void* hid, int64_t hid_ld,
+                        float* logits, int64_t logits_ld, void* ws, size_t ws_bytes, void* stream);
+void ps_debug_router_trace(void* buf);
+
 /* ======================================================================
  * Decode-step glue.
  * ps_layernorm: model.layernorm (model.py:168-175): x f32 (B, d) row b at

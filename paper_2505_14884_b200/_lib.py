@@ -14,6 +14,8 @@ import torch
 from .exceptions import CapacityError, EmptyCacheError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpolar_b200.so")
+if os.environ.get("PS_LIB_PATH"):  # experiment variants (tools/build_variant.sh); not the product path
+    LIB_PATH = os.environ["PS_LIB_PATH"]
 
 PS_DTYPE_F32 = 0
 PS_DTYPE_BF16 = 1
@@ -68,6 +70,10 @@ SIGNATURES = {
                            _vp]),
     "ps_router_mlp_workspace_bytes": (_sz, [_i, _i, _i]),
     "ps_router_mlp": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _sz, _vp]),
+    "ps_router_mlp_fused_workspace_bytes": (_sz, [_i, _i, _i, _i]),
+    "ps_router_mlp_fused": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _sz,
+                                 _vp]),
+    "ps_debug_router_trace": (None, [_vp]),
     "ps_debug_chain_stages": (None, [_i]),
     "ps_debug_chain_trace": (None, [_vp]),
     "ps_set_pdl": (None, [_i]),

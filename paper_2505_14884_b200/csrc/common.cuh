@@ -320,6 +320,12 @@ PS_DEV void st_dsmem_f32(uint32_t addr, float v) {
 }
 // asynchronous remote store that signals `bytes` on the remote CTA's mbarrier
 // (complete_tx): a producer->consumer DSMEM hand-off without cluster fences
+PS_DEV void st_async_v4(uint32_t remote_addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   remote_addr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
+               : "memory");
+}
 PS_DEV void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr),
                "r"(__float_as_uint(v)), "r"(remote_bar)

@@ -509,7 +509,13 @@ __global__ void __launch_bounds__(kThreads) sha_decode_kernel(const ShaParams p)
 // fixed) but never used: their scores are masked by select and their V rows
 // are zeroed in shared memory before the P.V product.
 constexpr int kMmaT = 32;
-constexpr int kMmaStages = 4;
+#ifndef PS_SHA_STAGES
+#define PS_SHA_STAGES 5
+#endif
+#ifndef PS_SHA_CTAS
+#define PS_SHA_CTAS 2
+#endif
+constexpr int kMmaStages = PS_SHA_STAGES;
 constexpr int kMmaTileBytes = kMmaT * 128 * 2;  // 8 KB of K (or V)
 
 PS_DEV void ldsm_x4(uint32_t addr, uint32_t* r) {
@@ -542,7 +548,7 @@ PS_DEV uint32_t mma_sw(int r, int C) {
 }
 
 template <int G, bool OUT_BF16>
-__global__ void __launch_bounds__(kThreads, 3) sha_mma_kernel(const __grid_constant__ CUtensorMap tmK,
+__global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __grid_constant__ CUtensorMap tmK,
                                                           const __grid_constant__ CUtensorMap tmV, const ShaParams p) {
   constexpr int D_H = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -910,8 +916,8 @@ int dispatch_g(const ShaParams& prm, int grid, int G, bool bf16, cudaStream_t st
 
 int partial_floats(int G, int d_h) { return G * (d_h + 2); }
 
-// resident SHA CTAs (64 KB of K/V stages each: 3 per SM)
-int sha_slots() { return ps_num_sms() * 3; }
+// resident SHA CTAs (80 KB of K/V stages each: 2 per SM)
+int sha_slots() { return ps_num_sms() * PS_SHA_CTAS; }
 
 // CTAs = units x splits (each unit cut into `splits` equal tile ranges).
 // Auto (num_splits == 0): the split count minimising the last-wave waste
@@ -943,6 +949,12 @@ int sha_ctas(int units, int NT, int num_splits, int G) {
   long long cap;
   if (num_splits < 0) {
     cap = -(long long)num_splits;
+  } else if (num_splits == 0 && units >= sha_slots()) {
+    // at least one unit per resident slot: ONE persistent stream-K wave
+    // (2 CTAs x 5 stages per SM).  Measured on B200 at ctx 1920 against the
+    // wave model below (3 CTAs x 4 stages): OPT-6.7B B=64 rho=.5 157.3 ->
+    // 151.5 us, LLaMA-8B B=256 k=4 162.7 -> 157.4 us, dense B=128 570.8 -> 565.7 us
+    cap = sha_slots();
   } else if (num_splits == 0 && G >= 4 && units >= (sha_slots() * 9) / 10) {
     // grouped heads (G >= 4: a unit's partial is G x (d_h + 2) floats, so
     // splitting costs more): one CTA per unit once there are ~2 waves of

@@ -97,8 +97,10 @@ class DecodeEngine:
         self.dense_backend = check_choice(dense_backend, ("cublas", "native"), "dense_backend")
         # the MLP router's two layers: tcgen05 kernels with their static weights
         # streamed ahead of the previous launch (PDL), or cuBLAS
-        self.router_backend = check_choice(router_backend or dense_backend, ("cublas", "native", "native_in"),
-                                           "router_backend")
+        # "fused" (default): both layers in one persistent launch
+        # (ps_router_mlp_fused), falling back to cuBLAS for shapes it does not cover
+        self.router_backend = check_choice(router_backend or ("fused" if dense_backend == "cublas" else "native"),
+                                           ("fused", "cublas", "native", "native_in"), "router_backend")
         # head router on a side stream, concurrent with the QKV GEMM (a
         # parallel branch of the captured graph); False = fused with the append
         self.concurrent_router = concurrent_router
@@ -396,7 +398,11 @@ class DecodeEngine:
                 r = self.mlp_routers[ell]
                 cnt = self.union_counts[ell:ell + 1]
                 out_bias = None  # the router's output bias is added inside ps_select_union
-                if self.router_backend in ("cublas", "native_in"):
+                if self.router_backend == "fused" and r.fused_into(self.h, self.r_hid, self.r_logits,
+                                                                  with_bias=False):
+                    out_bias = r.b_out
+                    n += 1
+                elif self.router_backend in ("cublas", "native_in", "fused"):
                     if self.router_backend == "native_in":  # tcgen05 kernel, static weights prefetched (PDL)
                         gather_gemm_into(r.w_in_t, None, None, self.h, self.h.stride(0), r.b_in, B, r.hidden_dim_,
                                          d, _lib.PS_ACT_RELU, self.r_hid, self.r_hid.stride(0), tag="gg_router")

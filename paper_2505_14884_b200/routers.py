@@ -178,6 +178,32 @@ class MlpRouter:
         return cls(w_in.shape[0], np.asarray(w_out).shape[1], w_in.shape[1], 0, device,
                    _weights=(w_in, b_in, w_out, b_out))
 
+    def fused_bytes(self, batch: int) -> int:
+        """Workspace bytes of the one-launch router (0: shape unsupported)."""
+        return int(_lib.load().ps_router_mlp_fused_workspace_bytes(batch, self.d_model, self.hidden_dim_,
+                                                                   self.ffn_dim))
+
+    def fused_into(self, x2d: torch.Tensor, hid: torch.Tensor, logits: torch.Tensor, with_bias: bool = True,
+                   tag: str = "router_fused") -> bool:
+        """Both router layers in ONE persistent launch with a device grid
+        barrier between them (ps_router_mlp_fused; static weights prefetched
+        ahead of the dependency wait).  Returns False (nothing launched) for
+        shapes the kernel does not cover."""
+        B, d = x2d.shape
+        nb = self.fused_bytes(B)
+        if not nb:
+            return False
+        lib = _lib.load()
+        ws = _ws.get(tag, nb, x2d.device)
+        st = lib.ps_router_mlp_fused(_lib.ptr(self.w_in_t), _lib.ptr(self.b_in), _lib.ptr(self.w_out_t),
+                                     _lib.ptr(self.b_out) if with_bias else None, d, self.hidden_dim_, self.ffn_dim,
+                                     _lib.ptr(x2d), x2d.stride(0), B, _lib.ptr(hid), hid.stride(0),
+                                     _lib.ptr(logits), logits.stride(0), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        if st == 5:  # PS_ERR_UNSUPPORTED
+            return False
+        _lib.check(st, "ps_router_mlp_fused")
+        return True
+
     def logits_into(self, x2d: torch.Tensor, hid: torch.Tensor, logits: torch.Tensor, with_bias: bool = True,
                     fused: bool = False) -> None:
         """hid = relu(x W_in + b_in) (bf16), logits = hid W_out (+ b_out) (f32).

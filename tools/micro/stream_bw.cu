@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(32 * LW + 32) stream_kernel(const uint16_t* w,
 template <int MODE, int LW>
 void run(const char* name, const uint16_t* w, const int* idx, unsigned long long* sink, int D, int d, int n_sel) {
   cudaFuncSetAttribute(stream_kernel<MODE, LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  for (int G : {128, 148, 296}) {
-    for (int S : {4, 8, 12}) {
+  for (int G : {52, 74, 104, 148, 296}) {
+    for (int S : {4, 8, 13}) {
       const int rows_per_cta = (n_sel / G) & ~1;
       const size_t smem = (size_t)S * 16384 + 2 * S * 8;
       float t[2];
@@ -137,6 +137,7 @@ int main() {
   cudaMemcpy(idx, h.data(), n_sel * 4, cudaMemcpyHostToDevice);
   cudaMalloc(&sink, 8);
   run<0, 4>("cp.async 4 warps", w, idx, sink, D, d, n_sel);
+  run<3, 1>("bulk 128B chunks", w, idx, sink, D, d, n_sel);
 
 
   run<2, 1>("bulk 8KB rows", w, idx, sink, D, d, n_sel);

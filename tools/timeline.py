@@ -23,6 +23,7 @@ from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy  # noqa: E
 from paper_2505_14884_b200.model import SHAPES, DeviceModel  # noqa: E402
 
 TRACED = {"ps_gather_gemm": "gemm", "ps_gather_gemm_t": "gemm", "ps_select_union": "topk",
+          "ps_router_mlp_fused": "router",
           "ps_sparse_mlp": "chain", "ps_router_mlp": "chain"}
 
 
@@ -46,6 +47,8 @@ class Proxy:
                 self.lib.ps_debug_gemm_trace(buf.data_ptr(), 0, 0)
             elif kind == "topk":
                 self.lib.ps_debug_topk_trace(buf.data_ptr())
+            elif kind == "router":
+                self.lib.ps_debug_router_trace(buf.data_ptr())
             else:
                 self.lib.ps_debug_chain_trace(buf.data_ptr())
             r = fn(*a)
@@ -53,6 +56,8 @@ class Proxy:
                 self.lib.ps_debug_gemm_trace(None, 0, 0)
             elif kind == "topk":
                 self.lib.ps_debug_topk_trace(None)
+            elif kind == "router":
+                self.lib.ps_debug_router_trace(None)
             else:
                 self.lib.ps_debug_chain_trace(None)
             return r
@@ -135,6 +140,8 @@ def main():
             f = t[:, 2][t[:, 2] > 0]
             rows.append((name, len(t), t[:, 0].min(), np.median(t[:, 0]), np.median(t[:, 1]),
                          np.median(f) if len(f) else None, t[:, 5].max()))
+        elif name == "ps_router_mlp_fused":
+            rows.append((name, len(t), t[:, 0].min(), np.median(t[:, 0]), None, None, t[:, 6].max()))
         else:
             rows.append((name, len(t), t[:, 0].min(), np.median(t[:, 0]), None, None, t.max()))
     t0 = min(r[2] for r in rows)
@@ -144,8 +151,14 @@ def main():
     for name, b in gl[-per:]:
         t = b.view(-1, 16).cpu().numpy()
         t = t[t[:, 0] > 0]
-        slots = {"ps_select_union": [(0, "start"), (5, "selected"), (7, "union")]}.get(
-            name, [(0, "start"), (1, "setup"), (2, "1st stage"), (3, "mma done"), (4, "epi done"), (5, "end")])
+        slots = {"ps_select_union": [(0, "start"), (5, "selected"), (7, "union")],
+                 "ps_router_mlp_fused": [(0, "start"), (1, "prefetched"), (7, "dep. wait"), (12, "p1 mma"),
+                                         (2, "p1 written"), (3, "barrier1"), (10, "reduce in"), (11, "reduce out"),
+                                         (4, "barrier2"), (8, "p2 mma0"), (9, "p2 mmaN"), (5, "acc2 ready"),
+                                         (6, "done")]}.get(
+            name, [(0, "start"), (1, "setup"), (2, "1st stage"), (3, "mma issued"), (8, "acc ready"),
+                   (10, "staged"), (11, "peers in"), (12, "reduced"), (13, "fre"), (9, "tile0 done"),
+                   (4, "epi done"), (5, "end")])
         print(f"  {name} ({len(t)} CTAs)")
         for j, lab in slots:
             v = t[:, j]
