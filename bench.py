@@ -86,7 +86,7 @@ def parse(argv=None):
     ap.add_argument("--distinct-layers", type=int, default=0,
                     help="TP: distinct weight sets cycled over the layers (0 = all distinct)")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = the workload batch)")
-    ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "native", "native_in"])
+    ap.add_argument("--router-backend", default=None, choices=[None, "cublas", "fused", "native", "native_in"])
     ap.add_argument("--kv-page-rows", type=int, default=0,
                     help="paged KV caches with this many rows per page (0 = contiguous)")
     ap.add_argument("--kv-reserve", default="full", choices=["full", "on_demand"],

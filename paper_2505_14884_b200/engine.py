@@ -97,9 +97,10 @@ class DecodeEngine:
         self.dense_backend = check_choice(dense_backend, ("cublas", "native"), "dense_backend")
         # the MLP router's two layers: tcgen05 kernels with their static weights
         # streamed ahead of the previous launch (PDL), or cuBLAS
-        # "fused" (default): both layers in one persistent launch
-        # (ps_router_mlp_fused), falling back to cuBLAS for shapes it does not cover
-        self.router_backend = check_choice(router_backend or ("fused" if dense_backend == "cublas" else "native"),
+        # "fused": both layers in one persistent launch (ps_router_mlp_fused),
+        # falling back to cuBLAS for shapes it does not cover (measured 2.5 %
+        # slower than cuBLAS per step at OPT-6.7B B=64, so not the default)
+        self.router_backend = check_choice(router_backend or dense_backend,
                                            ("fused", "cublas", "native", "native_in"), "router_backend")
         # head router on a side stream, concurrent with the QKV GEMM (a
         # parallel branch of the captured graph); False = fused with the append
