@@ -83,6 +83,8 @@ def parse(argv=None):
     ap.add_argument("--no-extra", action="store_true", help="skip the extra driver-observed configs")
     ap.add_argument("--dp", action="store_true", help="N > 1: data-parallel replicas instead of TP")
     ap.add_argument("--tp", action="store_true", help="(default for N > 1) tensor parallelism over the ranks")
+    ap.add_argument("--tp-collective", default="nccl", choices=["nccl", "p2p"],
+                    help="TP exchange: NCCL all-reduce, or the fused peer-memory all-reduce + residual add")
     ap.add_argument("--distinct-layers", type=int, default=0,
                     help="TP: distinct weight sets cycled over the layers (0 = all distinct)")
     ap.add_argument("--cpu-batch", type=int, default=0, help="batch of the CPU sample (0 = the workload batch)")
@@ -416,7 +418,10 @@ class Setup:
             from paper_2505_14884_b200.parallel import TPPlan, TensorParallel, random_shard
 
             plan = TPPlan.make(cfg, world, rank)
-            self.tp = TensorParallel(plan)
+            import torch.distributed as dist
+
+            self.tp = TensorParallel(plan, dist.group.WORLD if world > 1 else None,
+                                     collective=getattr(args, "tp_collective", "nccl"))
             self.model = model or random_shard(cfg, plan, seed=1234, device=dev,
                                                distinct_layers=args.distinct_layers or None)
             self.H_loc, self.Hkv_loc, self.D_loc = plan.heads_local, plan.kv_heads_local, plan.ffn_local

@@ -300,6 +300,21 @@ int ps_router_mlp_fused(const void* w_in_rows, const float* b_in, const void* w_
 void ps_debug_router_trace(void* buf);
 
 /* ======================================================================
+ * Tensor-parallel exchange.
+ * ps_allreduce_add_bf16: x (f32 (B, d), row stride x_ld) += sum over the
+ *   `world` ranks of their bf16 (B, d) partials, in ONE launch over peer
+ *   memory -- replaces dist.all_reduce(partial) + x.add_(partial) after the
+ *   O- and down-projections (parallel.py).  bufs / flags: device arrays of
+ *   the ranks' partial buffers (this call's slot) and inbox addresses
+ *   (CUDA IPC mappings); inbox: this rank's 8 uint32 flags; state: 2 uint32
+ *   (device epoch, ticket), zero-initialised once.  Callers alternate two
+ *   partial buffers from call to call (collective.P2PAllReduce).
+ * ==================================================================== */
+int ps_allreduce_add_bf16(const unsigned long long* bufs, const unsigned long long* flags, unsigned int* inbox,
+                          unsigned int* state, int rank, int world, int B, int d, float* x, int64_t x_ld,
+                          void* stream);
+
+/* ======================================================================
  * Decode-step glue.
  * ps_layernorm: model.layernorm (model.py:168-175): x f32 (B, d) row b at
  *   +b*x_ld -> y bf16 (B, d), eps 1e-5, f32 statistics.

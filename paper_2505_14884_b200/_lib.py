@@ -74,6 +74,7 @@ SIGNATURES = {
     "ps_router_mlp_fused": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _sz,
                                  _vp]),
     "ps_debug_router_trace": (None, [_vp]),
+    "ps_allreduce_add_bf16": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _i64, _vp]),
     "ps_debug_chain_stages": (None, [_i]),
     "ps_debug_chain_trace": (None, [_vp]),
     "ps_set_pdl": (None, [_i]),

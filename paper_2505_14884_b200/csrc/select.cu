@@ -834,6 +834,21 @@ int launch_topk(TopkParams prm, cudaStream_t st) {
       return PS_ERR_CUDA;
     configured = 1;
   }
+  if (prm.coresident) {
+    // grid-barrier union: a cooperative launch guarantees co-residency
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(prm.rows);
+    cfg.blockDim = dim3(kTopkThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, topk_rows_kernel, prm) != cudaSuccess) return PS_ERR_CUDA;
+    return launch_status();
+  }
   return launch_ex(topk_rows_kernel, dim3(prm.rows), dim3(kTopkThreads), smem, st, 1, prm);
 }
 
@@ -1151,6 +1166,10 @@ int select_union_v2(const float* logits, const float* bias, int rows, int cols, 
 int select_union_v2_max_cols();
 }  // namespace ps
 static int g_topk_v2 = -1;  // -1: from env PS_TOPK_V2 (default 1)
+static const int g_topk_coop = [] {
+  const char* e = getenv("PS_TOPK_COOP");
+  return e ? atoi(e) : 0;
+}();
 extern "C" void ps_debug_topk_v2(int enable) { g_topk_v2 = enable ? 1 : 0; }
 
 extern "C" int ps_select_union(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k,
@@ -1179,7 +1198,10 @@ extern "C" int ps_select_union(const float* logits, const float* bias, int rows,
   prm.bias = bias;
   // one CTA per row and per SM (the kernel's shared memory): all resident
   // at once iff rows <= SMs, and every CTA owns <= 512 words
-  prm.coresident = rows <= ps_num_sms() && (cols + 31) / 32 <= (size_t)kUnionWPT * kTopkThreads;
+  // the grid-barrier union needs every row CTA resident at once, which a
+  // plain launch does not guarantee: it is used only under a cooperative
+  // launch (PS_TOPK_COOP=1); otherwise the ticketed group union (no waits)
+  prm.coresident = g_topk_coop && rows <= ps_num_sms() && (cols + 31) / 32 <= (size_t)kUnionWPT * kTopkThreads;
   prm.tickets = reinterpret_cast<int*>(base);
   prm.group_bits = reinterpret_cast<uint32_t*>(base + head);
   prm.row_bits = prm.group_bits + su_groups(rows) * su_words(cols);

@@ -169,9 +169,17 @@ def random_shard(cfg: TransformerConfig, plan: TPPlan, seed: int = 0, scale: flo
 class TensorParallel:
     """Device hooks used by DecodeEngine(tp=...)."""
 
-    def __init__(self, plan: TPPlan, group=None):
+    def __init__(self, plan: TPPlan, group=None, collective: str = "nccl"):
+        """``collective``: "nccl" (torch.distributed all-reduce, then x += sum)
+        or "p2p" (collective.P2PAllReduce: one peer-memory kernel that waits
+        for every rank's bf16 partial and adds the sum into x; its IPC handles
+        travel over ``group``, which may be gloo)."""
+        if collective not in ("nccl", "p2p"):
+            raise ValueError(f"collective must be 'nccl' or 'p2p', got {collective!r}")
         self.plan = plan
         self.group = group
+        self.collective = collective
+        self._p2p = None
         self.heads_local = plan.heads_local
         self.kv_heads_local = plan.kv_heads_local
         self.group_base = plan.group_base
@@ -190,10 +198,28 @@ class TensorParallel:
                 return
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
+    def _p2p_engine(self, eng):
+        if self._p2p is None:
+            from .collective import P2PAllReduce
+
+            self._p2p = P2PAllReduce(self.group, self.plan.rank, self.plan.world, eng.x.numel(), eng.x.device)
+        return self._p2p
+
+    def reduce_into(self, eng, part) -> None:
+        """eng.x += sum over ranks of ``part`` (this rank's bf16 partial)."""
+        if self.collective == "p2p":
+            self._p2p_engine(eng).add_into(eng.x)
+            return
+        self.all_reduce(part)
+        eng.x.add_(part)
+
     def _partial(self, eng, name):
         """bf16 (B, d) buffer for a rank's partial residual update: the
         all-reduce moves half the bytes of f32 partials (SURVEY.md §8(e)
-        budgets bf16); the sum is added into the f32 residual stream."""
+        budgets bf16); the sum is added into the f32 residual stream.  With
+        the p2p collective it is the peer-mapped buffer of the next call."""
+        if self.collective == "p2p":
+            return self._p2p_engine(eng).next_buffer(eng.x.shape)
         t = self._tmp.get(name)
         if t is None:
             t = torch.zeros(eng.x.shape, dtype=torch.bfloat16, device=eng.x.device)
@@ -204,8 +230,7 @@ class TensorParallel:
         """x += all_reduce(attn_local @ W_o[local rows] (+ b_o on rank 0))."""
         part = self._partial(eng, "o")
         n = eng._linear_bf16(eng.attn, lw.w_o_t, lw.b_o, part, tag="gg_o")
-        self.all_reduce(part)
-        eng.x.add_(part)
+        self.reduce_into(eng, part)
         return n
 
     def mlp(self, eng, lw, idx, cnt, ell: int = 0) -> int:
@@ -232,6 +257,5 @@ class TensorParallel:
                 torch.addmm(eng._bf(mk.b2), hid, mk.w2t, out=part)
             else:
                 torch.mm(hid, mk.w2t, out=part)
-        self.all_reduce(part)
-        eng.x.add_(part)
+        self.reduce_into(eng, part)
         return n

@@ -55,3 +55,99 @@ def test_reference_engine_on_gpu_kernels(kv_heads):
     ref2, _ = _run(model, tokens, 1, forced=forced, **kw)
     rel = np.linalg.norm(got - ref2) / np.linalg.norm(ref2)
     assert rel <= 2e-2, rel
+
+
+def _import_reference():
+    import os
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "sparsedecode")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import sparsedecode
+    except Exception:
+        return None
+    return sparsedecode
+
+
+def test_unmodified_reference_engine_on_gpu_kernels():
+    """adapter.install on the REAL reference engine module
+    (sparsedecode.engine, pip-installed unmodified into baseline/_ref): its
+    own decode_step runs on this package's CUDA kernels and agrees with its
+    own CPU run (forced onto the same selections through the reference's
+    rebinding hook, tests/test_engine.py:55-64)."""
+    sd = _import_reference()
+    if sd is None:
+        pytest.skip("baseline/_ref (the unmodified reference install) is not present")
+    from sparsedecode import engine as sde, model as sdm
+
+    from paper_2505_14884_b200 import adapter
+
+    cfg = sdm.TransformerConfig(2, 128, 512, 8, 4, 256, 96, "relu")
+    model = sdm.random_model(cfg, 5)
+
+    def session(seed):
+        rng = np.random.default_rng(seed)
+        caches = []
+        for _ in range(2):
+            c = sd.KVCache(8, 4, 96, 16)
+            c.fill_random(rng, 40)
+            caches.append(c)
+        policy = sd.SparsityPolicy(mode="polar", mlp_k_table=sd.LayerKTable(((0, 64, 1.0), (1, 64, 1.0))),
+                                   head_density=0.5)
+        return sd.DecodeSession(caches=caches, policy=policy,
+                                mlp_routers=[sd.MlpRouter(128, 512, seed=70 + e) for e in range(2)],
+                                head_routers=[sd.HeadRouter(128, 4, seed=60 + e) for e in range(2)])
+
+    tokens = np.arange(8) * 3
+    BHI = sde.BatchHeadIndex
+
+    class _Heads:  # records / replays the head selections (BatchHeadIndex.from_logits)
+        full = staticmethod(BHI.full)
+        replay = None
+
+        @staticmethod
+        def from_logits(logits, k):
+            if _Heads.replay is not None:
+                return next(_Heads.replay)
+            out = BHI.from_logits(logits, k)
+            seen["bhi"].append(out)
+            return out
+
+    # record the selections of the GPU run, then replay them on the CPU run
+    seen = {"heads": [], "union": [], "bhi": []}
+    saved = adapter.install(sde)
+    try:
+        topk, union = sde.topk_indices_rows, sde.union_neuron_indices
+
+        def spy_topk(scores, k):
+            out = topk(scores, k)
+            seen["heads"].append(np.asarray(out))
+            return out
+
+        def spy_union(sets, layer=0):
+            out = union(sets, layer)
+            seen["union"].append(np.asarray(out))
+            return out
+        sde.topk_indices_rows, sde.union_neuron_indices = spy_topk, spy_union
+        sde.BatchHeadIndex = _Heads
+        got = sde.decode_step(session(1), model, tokens)
+    finally:
+        adapter.uninstall(sde, saved)
+        sde.BatchHeadIndex = BHI
+    assert sde.gqa_selective_attention_decode is saved["gqa_selective_attention_decode"]
+    assert seen["union"] and seen["bhi"], "the reference engine did not route through the installed kernels"
+    it_h, it_u = iter(seen["heads"]), iter(seen["union"])
+    orig_topk, orig_union = sde.topk_indices_rows, sde.union_neuron_indices
+    try:
+        sde.topk_indices_rows = lambda scores, k: next(it_h)
+        sde.union_neuron_indices = lambda sets, layer=0: next(it_u)
+        _Heads.replay = iter(seen["bhi"])
+        sde.BatchHeadIndex = _Heads
+        ref = sde.decode_step(session(1), model, tokens)
+    finally:
+        sde.topk_indices_rows, sde.union_neuron_indices = orig_topk, orig_union
+        sde.BatchHeadIndex = BHI
+    rel = np.linalg.norm(np.asarray(got) - np.asarray(ref)) / np.linalg.norm(np.asarray(ref))
+    assert rel <= 2e-2, rel

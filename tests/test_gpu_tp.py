@@ -137,7 +137,7 @@ def selections_from_trace(eng, plan, world):
     return heads, unions
 
 
-def _rank(rank, world, port, kv_heads, mode, q):
+def _rank(rank, world, port, kv_heads, mode, q, collective="nccl"):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -150,7 +150,8 @@ def _rank(rank, world, port, kv_heads, mode, q):
         L, d, D, H, V, S = CFG
         cfg = TransformerConfig(L, d, D, H, kv_heads, V, S, "relu")
         plan = TPPlan.make(cfg, world, rank)
-        eng, tokens = _build(kv_heads, mode, tp=TensorParallel(plan), plan=plan)
+        eng, tokens = _build(kv_heads, mode, tp=TensorParallel(plan, dist.group.WORLD, collective=collective),
+                             plan=plan)
         eng.record = {}
         logits = eng.step(tokens).cpu().numpy()
         heads, unions = _selections(eng, plan, world)
@@ -162,14 +163,19 @@ def _rank(rank, world, port, kv_heads, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kv_heads,mode", [(8, "polar"), (2, "polar"), (8, "dense")])
-def test_tp2_device_matches_oracle(kv_heads, mode):
+@pytest.mark.parametrize("kv_heads,mode,collective", [(8, "polar", "nccl"), (2, "polar", "nccl"),
+                                                     (8, "dense", "nccl"), (8, "polar", "p2p"),
+                                                     (2, "polar", "p2p")])
+def test_tp2_device_matches_oracle(kv_heads, mode, collective):
+    """collective "nccl": the torch.distributed all-reduce (gloo here: the
+    ranks share one GPU); "p2p": the fused peer-memory all-reduce + residual
+    add (ps_allreduce_add_bf16) over CUDA IPC mappings."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_rank, args=(r, 2, port, kv_heads, mode, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank, args=(r, 2, port, kv_heads, mode, q, collective)) for r in range(2)]
     for p in ps:
         p.start()
     for p in ps:
