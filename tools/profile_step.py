@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--ctx", type=int, default=1920)
     ap.add_argument("--rho", type=float, default=0.5)
     ap.add_argument("--union", type=float, default=0.5)
+    ap.add_argument("--k-frac", type=float, default=0.1)
+    ap.add_argument("--hot-frac", type=float, default=0.072)
+    ap.add_argument("--union-recipe", default="hot-cold", choices=["hot-cold", "hot-set"])
     ap.add_argument("--mode", default="polar")
     ap.add_argument("--layers", type=int, default=0, help="truncate to this many layers (0 = all)")
     ap.add_argument("--no-graph", action="store_true")
@@ -42,7 +45,9 @@ def main():
     if a.layers:
         cfg = dataclasses.replace(cfg, layers=a.layers)
     L, H_kv, D = cfg.layers, cfg.kv_heads, cfg.ffn_dim
-    k_mlp = max(1, int(round(a.union * D)))
+    import bench  # the bench's neuron recipe (hot/cold by default)
+
+    k_mlp, n_hot = bench.neuron_recipe(a, D)
     gen = np.random.default_rng(7)
     model = DeviceModel.random(cfg, seed=1234, device=dev)
     relu = cfg.activation == "relu"
@@ -50,7 +55,8 @@ def main():
     mr = None
     if relu:
         mr = [pb.MlpRouter.random_device(cfg.model_dim, D, seed=200 + e, device=dev,
-                                         hot=gen.choice(D, k_mlp, replace=False)) for e in range(L)]
+                                         hot=gen.choice(D, n_hot, replace=False) if n_hot else None,
+                                         center=a.union_recipe == "hot-cold") for e in range(L)]
     if a.mode == "polar":
         pol = SparsityPolicy(mode="polar", head_density=a.rho,
                              mlp_k_table={e: k_mlp for e in range(L)} if relu else None)
