@@ -98,8 +98,11 @@ class DecodeEngine:
         # the MLP router's two layers: tcgen05 kernels with their static weights
         # streamed ahead of the previous launch (PDL), or cuBLAS
         # "fused": both layers in one persistent launch (ps_router_mlp_fused),
-        # falling back to cuBLAS for shapes it does not cover (measured 2.5 %
-        # slower than cuBLAS per step at OPT-6.7B B=64, so not the default)
+        # falling back to cuBLAS for shapes it does not cover.  Default: fused
+        # for B <= 8 (OPT-6.7B B=1: 3.626 -> 3.584 ms per step), cuBLAS above
+        # (B=16: 5.163 vs 5.211 ms, B=64: 2.5 % faster than fused)
+        if router_backend is None and dense_backend == "cublas" and batch <= 8:
+            router_backend = "fused"
         self.router_backend = check_choice(router_backend or dense_backend,
                                            ("fused", "cublas", "native", "native_in"), "router_backend")
         # head router on a side stream, concurrent with the QKV GEMM (a
