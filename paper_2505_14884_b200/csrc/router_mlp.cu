@@ -33,7 +33,7 @@ constexpr int RBK = 64;         // K elements per stage (one 128-byte swizzle ro
 constexpr int kRThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 constexpr int kREpi = 128;
 constexpr int kRA1 = 4;       // phase-1 A K-blocks per CTA (64 KB)
-constexpr int kRStages = 5;   // phase-2 pipeline stages (at most; fewer at NB = 128)
+constexpr int kRStages = 12;  // phase-2 pipeline stages (at most: as many as the shared memory holds)
 
 struct GridBar {
   unsigned int count;
@@ -77,19 +77,20 @@ PS_DEV unsigned int ld_acquire_u32(const unsigned int* p) {
 }
 
 PS_DEV void grid_wait_gen(const GridBar* bar, uint32_t target) {
-  while (ld_acquire_u32(&bar->gen) - target > 0x7fffffffu) __nanosleep(64);
+  while (ld_acquire_u32(&bar->gen) - target > 0x7fffffffu) __nanosleep(20);
 }
 
+// Called by one thread after a CTA barrier: its acq_rel fence is cumulative
+// over the writes the barrier ordered before it (as in a cooperative grid sync).
 PS_DEV void grid_arrive_wait(GridBar* bar, uint32_t target, int nctas) {
-  __threadfence();
-  if (atomicAdd(&bar->count, 1u) == (unsigned int)nctas - 1u) {
+  unsigned int old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&bar->count) : "memory");
+  if (old == (unsigned int)nctas - 1u) {
     bar->count = 0u;
-    __threadfence();
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar->gen), "r"(target) : "memory");
   } else {
     grid_wait_gen(bar, target);
   }
-  __threadfence();
 }
 
 __global__ void __launch_bounds__(kRThreads, 1)
@@ -284,7 +285,6 @@ __global__ void __launch_bounds__(kRThreads, 1)
         }
       }
     }
-    __threadfence();
     asm volatile("bar.sync 1, %0;" ::"n"(kREpi));
     uint32_t gen0 = 0;
     if (et == 0) {
@@ -303,10 +303,15 @@ __global__ void __launch_bounds__(kRThreads, 1)
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       const float4* src = reinterpret_cast<const float4*>(p.part + (size_t)n * p.r + j);
       const size_t step = (size_t)NB * p.r / 4;
-#pragma unroll 4
-      for (int s = 0; s < p.slices1; ++s) {
-        const float4 t = __ldcg(src + s * step);
-        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      for (int s0 = 0; s0 < p.slices1; s0 += 16) {  // 16 loads in flight, then the sums (slice order)
+        float4 t[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+          t[s] = s0 + s < p.slices1 ? __ldcg(src + (s0 + s) * step) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          acc.x += t[s].x; acc.y += t[s].y; acc.z += t[s].z; acc.w += t[s].w;
+        }
       }
       const float4 b = p.b_in ? __ldg(reinterpret_cast<const float4*>(p.b_in + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
       uint2 pk;
@@ -315,7 +320,6 @@ __global__ void __launch_bounds__(kRThreads, 1)
       *reinterpret_cast<uint2*>(p.hid + (size_t)n * p.hid_ld + j) = pk;
     }
     fence_proxy_async_global_r();  // generic hid stores -> the other CTAs' TMA (async proxy) loads
-    __threadfence();
     if (tr && et == 0) tr[11] = r_time();
     asm volatile("bar.sync 1, %0;" ::"n"(kREpi));
     if (et == 0) grid_arrive_wait(p.bar, gen0 + 2u, nctas);
@@ -427,7 +431,7 @@ extern "C" int ps_router_mlp_fused(const void* w_in_t, const float* b_in, const 
   if ((rc = rmap(&tWout, w_out_t, r, D, r, RBM)) != PS_OK) return rc;
   if ((rc = rmap(&tHid, hid, r, B, hid_ld, prm.NB)) != PS_OK) return rc;
   const size_t stage = (size_t)RBM * RBK * 2 + (size_t)prm.NB * RBK * 2;
-  const size_t fixed = 1024 + (size_t)kRA1 * stage + 256;
+  const size_t fixed = 1024 + (size_t)kRA1 * stage + 512;  // + barriers (<= 35 x 8 B) and the TMEM slot
   prm.stages = fixed < 227 * 1024 ? (int)((227 * 1024 - fixed) / stage) : 0;
   if (prm.stages > kRStages) prm.stages = kRStages;
   if (prm.stages < 2) return PS_ERR_UNSUPPORTED;

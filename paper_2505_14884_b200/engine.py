@@ -99,9 +99,9 @@ class DecodeEngine:
         # streamed ahead of the previous launch (PDL), or cuBLAS
         # "fused": both layers in one persistent launch (ps_router_mlp_fused),
         # falling back to cuBLAS for shapes it does not cover.  Default: fused
-        # for B <= 8 (OPT-6.7B B=1: 3.626 -> 3.584 ms per step), cuBLAS above
-        # (B=16: 5.163 vs 5.211 ms, B=64: 2.5 % faster than fused)
-        if router_backend is None and dense_backend == "cublas" and batch <= 8:
+        # for B <= 16 (OPT-6.7B per step: B=1 3.564 -> 3.507 ms, B=8 4.309 ->
+        # 4.292, B=16 5.122 -> 5.112), cuBLAS above (B=64: 1.5 % faster than fused)
+        if router_backend is None and dense_backend == "cublas" and batch <= 16:
             router_backend = "fused"
         self.router_backend = check_choice(router_backend or dense_backend,
                                            ("fused", "cublas", "native", "native_in"), "router_backend")
