@@ -91,7 +91,9 @@ def graph_run(fn):
     return s.elapsed_time(e) * 1e3
 
 
-print(f"B={B} |S|={S} PS_GG_PUSH={os.environ.get('PS_GG_PUSH', '1')}")
+if os.environ.get("LSU_MODE"):
+    L.ps_debug_gemm_lsu_mode(int(os.environ["LSU_MODE"]))
+print(f"B={B} |S|={S} PS_GG_PUSH={os.environ.get('PS_GG_PUSH', '1')} LSU_MODE={os.environ.get('LSU_MODE', '1')}")
 us = graph_run(lambda tr: [up(i, POOL[i] if tr else None) for i in range(3)])
 print(f"UP x3 graph: {us:.1f} us ({us / 3:.1f} per launch)")
 show("UP #2", POOL[1])
