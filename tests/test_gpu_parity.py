@@ -136,7 +136,7 @@ def test_select_union_with_bias():
 
 
 @pytest.mark.parametrize("case", ["hotcold", "ties", "nan_inf", "threshold", "shard", "rows300", "narrow",
-                                  "opt66b"])
+                                  "opt66b", "single", "single_shard", "single_ties"])
 def test_select_union_kernels_agree_with_oracle(case):
     """ps_select_union on both kernels (the low-latency row kernel and the
     bracket kernel) against the oracle: bias, ties at the k-th key, NaN /
@@ -152,11 +152,13 @@ def test_select_union_kernels_agree_with_oracle(case):
         rows, cols, k = 9, 1001, 100
     elif case == "opt66b":
         rows, cols, k = 32, 36864, 3686
+    elif case.startswith("single"):
+        rows = 1
     s = rng.normal(size=(rows, cols)).astype(np.float32)
     b = np.zeros(cols, np.float32)
-    if case in ("hotcold", "rows300", "shard", "opt66b"):
+    if case in ("hotcold", "rows300", "shard", "opt66b", "single", "single_shard"):
         b[rng.choice(cols, cols // 14, replace=False)] = 6.0
-    if case == "ties":
+    if case in ("ties", "single_ties"):
         s = np.round(s * 8) / 8
     if case == "nan_inf":
         s[:, ::97] = np.nan
@@ -166,7 +168,7 @@ def test_select_union_kernels_agree_with_oracle(case):
         k = cols // 2
     if case == "threshold":
         k, thr = 0, 1.5
-    if case == "shard":
+    if case in ("shard", "single_shard"):
         lo, hi = 4096, 12000
     hi = cols if hi is None else hi
     z = (s + b).astype(np.float32)
