@@ -494,8 +494,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PS_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 with a gloo
+    # group, so the TP path (sharding, graph capture with the p2p collective,
+    # the JSON line) runs end to end on a one-GPU box; its timings are meaningless
+    share = os.environ.get("PS_BENCH_SHARE_GPU") == "1" and world > 1
+    if share:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo", init_method="env://")
+        else:
+            dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tp_on = (world > 1 and not args.dp) or args.tp

@@ -58,3 +58,29 @@ def test_reference_arm_line():
              "--warmup", "1")
     assert j["impl"] == "reference" and j["value"] > 0
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["cpu_baseline"]["value"] == j["value"]
+
+
+def test_bench_tp2_path_on_a_shared_gpu():
+    """bench.py --gpus 2 (TP over two torchrun ranks) end to end on ONE GPU:
+    both ranks on cuda:0 (PS_BENCH_SHARE_GPU=1, gloo carries the handles), the
+    fused p2p exchange inside the captured step, rank 0 prints one line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, PS_BENCH_SHARE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--config", "tiny", "--batch", "8", "--ctx", "200", "--steps", "3",
+                          "--warmup", "3", "--tp-collective", "p2p", "--no-cpu", "--no-extra"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["scaling"] == "strong" and j["value"] > 0
+    assert j["config"]["parallelism"] == "tp2"
+    assert j["setup"]["graph_captured"] is True, j["setup"]
+    assert j["tp_load"] is not None and len(j["tp_load"]["selected_kv_units_per_rank"]) == 2
