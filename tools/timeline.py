@@ -76,6 +76,7 @@ def main():
     ap.add_argument("--union-recipe", default="hot-cold")
     ap.add_argument("--router-backend", default=None)
     ap.add_argument("--mlp-backend", default="split")
+    ap.add_argument("--dense-backend", default="cublas")
     ap.add_argument("--layers-shown", type=int, default=2)
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--dot", default="", help="dump the captured graph (cudaGraphDebugDotPrint) here")
@@ -94,7 +95,7 @@ def main():
                                      center=a.union_recipe == "hot-cold") for e in range(L)]
     pol = SparsityPolicy(mode="polar", head_density=a.rho, mlp_k_table={e: k_mlp for e in range(L)})
     eng = DecodeEngine(model, a.batch, a.ctx + 64, pol, head_routers=hr, mlp_routers=mr,
-                       router_backend=a.router_backend, mlp_backend=a.mlp_backend)
+                       router_backend=a.router_backend, mlp_backend=a.mlp_backend, dense_backend=a.dense_backend)
     eng.fill_random(a.ctx, seed=99)
     eng.tokens.copy_(torch.randint(0, cfg.vocab, (a.batch,), dtype=torch.int32))
     lib = _lib.load()
