@@ -78,6 +78,9 @@ int ps_num_sms(void);
  * ==================================================================== */
 /* debug: 0 forces the CUDA-core SHA path (d_h = 128 otherwise runs on mma.sync) */
 void ps_debug_sha_mma(int enable);
+/* debug: per-CTA globaltimer stamps of ps_sha_decode's tensor-core kernel
+ * (8 u64 per CTA: start, after the dependency wait, partition known, end); NULL = off */
+void ps_debug_sha_trace(void* buf);
 size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int top_k, int num_splits);
 int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_len);
 int ps_sha_decode(const void* q, int64_t q_ld,

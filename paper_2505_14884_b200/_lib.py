@@ -35,6 +35,7 @@ SIGNATURES = {
     "ps_status_string": (ctypes.c_char_p, [_i]),
     "ps_num_sms": (_i, []),
     "ps_debug_sha_mma": (None, [_i]),
+    "ps_debug_sha_trace": (None, [_vp]),
     "ps_sha_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
     "ps_sha_auto_splits": (_i, [_i, _i, _i, _i, _i]),
     "ps_sha_decode": (_i, [_vp, _i64, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _i,

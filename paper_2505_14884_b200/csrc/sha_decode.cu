@@ -80,6 +80,8 @@ struct ShaParams {
   int64_t out_ld;
   int* counters;
   float* partials;
+  unsigned long long* trace;  // debug (ps_debug_sha_trace): 8 u64 per CTA, NULL normally
+  int zero_inline;  // tensor-core kernel: the stream-K CTAs zero the unselected heads themselves (no B extra CTAs)
 };
 
 // Physical row of logical row `row0` of unit (b, g) in the row view of the
@@ -547,6 +549,14 @@ PS_DEV uint32_t mma_sw(int r, int C) {
   return (uint32_t)((C >> 3) * 4096 + r * 128 + (((C & 7) ^ (r & 7)) << 4));
 }
 
+PS_DEV unsigned long long sha_time() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SHA_STAMP(slot) \
+  do { if (p.trace && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * 8 + (slot)] = sha_time(); } while (0)
+
 template <int G, bool OUT_BF16>
 __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __grid_constant__ CUtensorMap tmK,
                                                           const __grid_constant__ CUtensorMap tmV, const ShaParams p) {
@@ -567,8 +577,21 @@ __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __
   const int n_units = p.B * p.top_k;
   // the B zero-fill CTAs come first (they overlap the main work instead of
   // forming a tail); stream-K CTA index = blockIdx.x - B
-  const int bid = (int)blockIdx.x - p.B;
+  // zero_inline: every CTA is a stream-K CTA (the unselected heads are zeroed
+  // below, while its first tiles are in flight); else the B zero-fill CTAs
+  // come first and stream-K CTA index = blockIdx.x - B
+  const int bid = p.zero_inline ? (int)blockIdx.x : (int)blockIdx.x - p.B;
+  SHA_STAMP(0);
+  // input-independent prologue before the dependency wait (overlaps the
+  // previous kernel's tail under PDL)
+  if (bid >= 0 && tid == 0) {
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    for (int s = 0; s < kMmaStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
   griddep_wait();
+  SHA_STAMP(1);
 
   if (bid < 0) {
     // ---- zero-fill CTA for sequence b: heads of non-selected groups = 0.0
@@ -598,12 +621,6 @@ __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __
   const int sel_first = __ldg(p.sel + u_first);
   const int len_first = __ldg(p.lengths + u_first / p.top_k);
   sha_len_partial(p, flag + 1);
-  if (tid == 0) {
-    prefetch_tmap(&tmK);
-    prefetch_tmap(&tmV);
-    for (int s = 0; s < kMmaStages; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
   __syncthreads();
   {
     const int nt = sha_nt(p, flag + 1, kMmaT);
@@ -659,8 +676,26 @@ __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __
   const int lrow = warp * 8 + (lane & 7);  // ldmatrix row supplied by this lane
   const int lmat = lane >> 3;              // ldmatrix matrix index
   const uint32_t sK_u = smem_u32(sK), sV_u = smem_u32(sV);
+  if (p.zero_inline) {
+    // heads of the groups a sequence did not select are 0.0 (sequences
+    // bid, bid + n_ctas, ...); red_o is free until the first unit epilogue
+    int* sel_flag = reinterpret_cast<int*>(red_o);
+    for (int b = bid; b < p.B; b += p.n_ctas) {
+      for (int g2 = tid; g2 < p.H_kv; g2 += kThreads) sel_flag[g2] = 0;
+      __syncthreads();
+      for (int j = tid; j < p.top_k; j += kThreads) {
+        const int g2 = p.sel[(size_t)b * p.top_k + j] - p.group_base;
+        if (g2 >= 0 && g2 < p.H_kv) sel_flag[g2] = 1;
+      }
+      __syncthreads();
+      for (int e = tid; e < p.H * D_H; e += kThreads)
+        if (!sel_flag[(e / D_H) / G]) store_out<OUT_BF16>(p.out, (size_t)b * p.out_ld + e, 0.0f);
+      __syncthreads();
+    }
+  }
   int it = 0;
   long long f = f0;
+  SHA_STAMP(2);
   while (f < f1) {
     const int NT = ld_nt(flag + 5);
     const int u = (int)(f / NT);
@@ -704,6 +739,7 @@ __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __
     for (int k2 = 0; k2 < nt_seg; ++k2, ++it) {
       const int stage = it % kMmaStages;
       mbar_wait(&bars[stage], (it / kMmaStages) & 1);
+      if (it == 0) SHA_STAMP(4);
       if (k2 < nt_real) {
         const int valid = min(kMmaT, len - (t0 + k2) * kMmaT);
         const uint32_t kbase = sK_u + stage * kMmaTileBytes, vbase = sV_u + stage * kMmaTileBytes;
@@ -834,6 +870,7 @@ __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __
     }
     __syncthreads();
   }
+  SHA_STAMP(3);
   griddep_launch();
 }
 
@@ -878,7 +915,13 @@ int launch_sha_mma(const ShaParams& prm, int grid, cudaStream_t st) {
   int rc = sha_tmap(&tk, prm.k, rows);
   if (rc == PS_OK) rc = sha_tmap(&tv, prm.v, rows);
   if (rc != PS_OK) return rc;
-  return launch_ex(kern, dim3(grid), dim3(kThreads), smem, st, 1, tk, tv, prm);
+  // the stream-K CTAs zero the unselected heads themselves: no B extra CTAs
+  // holding slots at the start (their stream-K neighbours started ~2 us late
+  // and finished last)
+  (void)grid;
+  ShaParams p2 = prm;
+  p2.zero_inline = 1;
+  return launch_ex(kern, dim3(prm.n_ctas), dim3(kThreads), smem, st, 1, tk, tv, p2);
 }
 
 int g_sha_mma = 1;  // 0: CUDA-core path for every shape (ps_debug_sha_mma)
@@ -989,6 +1032,8 @@ extern "C" size_t ps_sha_workspace_bytes(int B, int H, int H_kv, int d_h, int to
 }
 
 extern "C" void ps_debug_sha_mma(int enable) { g_sha_mma = enable ? 1 : 0; }
+static unsigned long long* g_sha_trace = nullptr;
+extern "C" void ps_debug_sha_trace(void* buf) { g_sha_trace = static_cast<unsigned long long*>(buf); }
 
 // 0 = stream-K over one resident wave (the default)
 extern "C" int ps_sha_auto_splits(int B, int H_kv, int d_h, int top_k, int max_len) {
@@ -1043,8 +1088,9 @@ static int sha_decode_impl(const void* q, int64_t q_ld, const void* k_cache, con
   prm.out = out;
   prm.out_ld = out_ld;
   prm.counters = static_cast<int*>(ws);
+  prm.trace = g_sha_trace;
   prm.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes);
-  const int grid = prm.n_ctas + B;
+  const int grid = prm.n_ctas + B;  // the CUDA-core kernel's B zero-fill CTAs (the tensor-core kernel zeroes inline)
   const bool bf16 = out_dtype == PS_DTYPE_BF16;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (d_h) {
