@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, PS_SHA_CTAS) sha_mma_kernel(const __
   const int lrow = warp * 8 + (lane & 7);  // ldmatrix row supplied by this lane
   const int lmat = lane >> 3;              // ldmatrix matrix index
   const uint32_t sK_u = smem_u32(sK), sV_u = smem_u32(sV);
-  if (p.zero_inline) {
+  if (p.zero_inline && p.top_k < p.H_kv) {  // every group selected (dense): nothing to zero
     // heads of the groups a sequence did not select are 0.0 (sequences
     // bid, bid + n_ctas, ...); red_o is free until the first unit epilogue
     int* sel_flag = reinterpret_cast<int*>(red_o);

@@ -23,7 +23,7 @@ from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy  # noqa: E
 from paper_2505_14884_b200.model import SHAPES, DeviceModel  # noqa: E402
 
 TRACED = {"ps_gather_gemm": "gemm", "ps_gather_gemm_t": "gemm", "ps_select_union": "topk",
-          "ps_router_mlp_fused": "router",
+          "ps_router_mlp_fused": "router", "ps_sha_decode": "sha",
           "ps_sparse_mlp": "chain", "ps_router_mlp": "chain"}
 
 
@@ -49,6 +49,8 @@ class Proxy:
                 self.lib.ps_debug_topk_trace(buf.data_ptr())
             elif kind == "router":
                 self.lib.ps_debug_router_trace(buf.data_ptr())
+            elif kind == "sha":
+                self.lib.ps_debug_sha_trace(buf.data_ptr())
             else:
                 self.lib.ps_debug_chain_trace(buf.data_ptr())
             r = fn(*a)
@@ -58,6 +60,8 @@ class Proxy:
                 self.lib.ps_debug_topk_trace(None)
             elif kind == "router":
                 self.lib.ps_debug_router_trace(None)
+            elif kind == "sha":
+                self.lib.ps_debug_sha_trace(None)
             else:
                 self.lib.ps_debug_chain_trace(None)
             return r
@@ -143,6 +147,10 @@ def main():
                          np.median(f) if len(f) else None, t[:, 5].max()))
         elif name == "ps_router_mlp_fused":
             rows.append((name, len(t), t[:, 0].min(), np.median(t[:, 0]), None, None, t[:, 6].max()))
+        elif name == "ps_sha_decode":
+            t8 = b.view(-1, 8).cpu().numpy()
+            t8 = t8[t8[:, 0] > 0]
+            rows.append((name, len(t8), t8[:, 0].min(), np.median(t8[:, 0]), None, None, t8[:, 3].max()))
         else:
             rows.append((name, len(t), t[:, 0].min(), np.median(t[:, 0]), None, None, t.max()))
     t0 = min(r[2] for r in rows)
@@ -150,9 +158,10 @@ def main():
     gl = [(n, b) for n, b in proxy.bufs if b.view(-1, 16)[:, 0].gt(0).any()]
     per = len(gl) // L
     for name, b in gl[-per:]:
-        t = b.view(-1, 16).cpu().numpy()
+        t = b.view(-1, 8 if name == "ps_sha_decode" else 16).cpu().numpy()
         t = t[t[:, 0] > 0]
         slots = {"ps_select_union": [(0, "start"), (5, "selected"), (7, "union")],
+                 "ps_sha_decode": [(0, "start"), (1, "dep wait"), (2, "partition"), (4, "1st tile"), (3, "end")],
                  "ps_router_mlp_fused": [(0, "start"), (1, "prefetched"), (7, "dep. wait"), (12, "p1 mma"),
                                          (2, "p1 written"), (3, "barrier1"), (10, "reduce in"), (11, "reduce out"),
                                          (4, "barrier2"), (8, "p2 mma0"), (9, "p2 mmaN"), (5, "acc2 ready"),
