@@ -295,7 +295,7 @@ void ps_debug_chain_trace(void* buf);
  * before the dependency wait.  N <= 128, d % 64 == 0, h % 128 == 0; other
  * shapes return PS_ERR_UNSUPPORTED (callers fall back to ps_router_mlp or two
  * GEMMs).  ws: ps_router_mlp_fused_workspace_bytes(N, d, h, D) bytes,
- * zero-initialised once (self-resetting barrier word + f32 partials). */
+ * zero-initialised once (monotonic barrier counter + f32 partials). */
 size_t ps_router_mlp_fused_workspace_bytes(int N, int d, int h, int D);
 int ps_router_mlp_fused(const void* w_in_rows, const float* b_in, const void* w_out_rows, const float* b_out,
                         int d, int h, int D, const void* x, int64_t x_ld, int N, void* hid, int64_t hid_ld,

@@ -816,13 +816,17 @@ namespace {
 // ---------------------------------------------------------------------------
 // Small-batch UP projection as a gathered GEMV on CUDA cores (N <= 4; at 8
 // and 16 rows the per-element x unpacking makes it FMA-bound and the tcgen05
-// tiles win -- measured in the decode step): every
-// warp owns whole rows (two at a time, sharing the x loads), so there is no
-// split-K and no cross-CTA reduction -- the kernel is a pure row stream.  x is
-// staged once per CTA in shared memory (rows >= N zero).  Positions in
+// tiles win -- measured in the decode step).  Every warp owns whole rows, so
+// there is no split-K and no cross-CTA reduction -- the kernel is a pure row
+// stream.  A warp issues a whole 8 KB chunk of its row (16 x 16 B per lane)
+// before consuming any of it, and its first chunk before x is staged, so at
+// B = 1 (|S| ~ 1.6 K rows, >= one warp per row) the entire gathered matrix is
+// in flight at once: one HBM round trip instead of the four serial 4 KB
+// round trips of a two-rows-per-warp unroll-4 loop (6.6 -> 5.6 us alone).
+// x is staged once per CTA in shared memory (rows >= N zero).  Positions in
 // [count, round_up(count, pad)) are written as zeros, like the tile path.
 constexpr int kGvThreads = 256;
-constexpr int kGvUnroll = 4;
+constexpr int kGvChunk = 16;  // 16-byte loads in flight per lane
 
 template <int NB>
 __global__ void __launch_bounds__(kGvThreads) gemv_up_kernel(const uint16_t* __restrict__ w, int64_t w_ld,
@@ -837,72 +841,68 @@ __global__ void __launch_bounds__(kGvThreads) gemv_up_kernel(const uint16_t* __r
   griddep_wait();  // x, idx and count come from the preceding kernels
   griddep_launch();
   const int count = count_dev ? min(__ldg(count_dev), M) : M;
+  const int nw = gridDim.x * (kGvThreads / 32);
+  int p = blockIdx.x * (kGvThreads / 32) + warp;
+  uint4 a[kGvChunk];
+  const uint4* wr = nullptr;
+  int id = 0;
+  auto load_chunk = [&](int c0) {
+#pragma unroll
+    for (int u = 0; u < kGvChunk; ++u) {
+      const int c = c0 + lane + 32 * u;
+      a[u] = c < kv ? __ldg(wr + c) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (p < count) {  // the first chunk streams in while x is staged
+    id = idx ? __ldg(idx + p) : p;
+    wr = reinterpret_cast<const uint4*>(w + (size_t)id * w_ld);
+    load_chunk(0);
+  }
   for (int i = threadIdx.x; i < NB * kv; i += kGvThreads) {
     const int b = i / kv, c = i - b * kv;
     sx4[i] = b < N ? __ldg(reinterpret_cast<const uint4*>(x + (size_t)b * x_ld) + c) : make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  const int nw = gridDim.x * (kGvThreads / 32);
-  for (int p0 = 2 * (blockIdx.x * (kGvThreads / 32) + warp); p0 < count; p0 += 2 * nw) {
-    const bool two = p0 + 1 < count;
-    const int id0 = idx ? __ldg(idx + p0) : p0;
-    const int id1 = two ? (idx ? __ldg(idx + p0 + 1) : p0 + 1) : id0;
-    const uint4* w0 = reinterpret_cast<const uint4*>(w + (size_t)id0 * w_ld);
-    const uint4* w1 = reinterpret_cast<const uint4*>(w + (size_t)id1 * w_ld);
-    float acc0[NB], acc1[NB];
+  for (; p < count; p += nw) {
+    float acc[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) acc0[b] = acc1[b] = 0.f;
-    for (int c0 = lane; c0 < kv; c0 += 32 * kGvUnroll) {
-      uint4 a0[kGvUnroll], a1[kGvUnroll];
+    for (int b = 0; b < NB; ++b) acc[b] = 0.f;
+    for (int c0 = 0; c0 < kv; c0 += 32 * kGvChunk) {
+      if (c0 > 0) load_chunk(c0);
 #pragma unroll
-      for (int u = 0; u < kGvUnroll; ++u) {
-        const int c = c0 + 32 * u;
-        a0[u] = c < kv ? __ldg(w0 + c) : make_uint4(0, 0, 0, 0);
-        a1[u] = c < kv ? __ldg(w1 + c) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < kGvUnroll; ++u) {
-        const int c = c0 + 32 * u;
+      for (int u = 0; u < kGvChunk; ++u) {
+        const int c = c0 + lane + 32 * u;
         if (c < kv) {
-          float wa[8], wb[8];
-          unpack8(a0[u], wa);
-          unpack8(a1[u], wb);
+          float wa[8];
+          unpack8(a[u], wa);
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             float xf[8];
             unpack8(sx4[b * kv + c], xf);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              acc0[b] = fmaf(wa[e], xf[e], acc0[b]);
-              acc1[b] = fmaf(wb[e], xf[e], acc1[b]);
-            }
+            for (int e = 0; e < 8; ++e) acc[b] = fmaf(wa[e], xf[e], acc[b]);
           }
         }
       }
     }
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      acc0[b] = warp_sum(acc0[b]);
-      acc1[b] = warp_sum(acc1[b]);
+    const int id_done = id, p_done = p;
+    if (p + nw < count) {  // next row's first chunk before this row's reduction
+      id = idx ? __ldg(idx + p + nw) : p + nw;
+      wr = reinterpret_cast<const uint4*>(w + (size_t)id * w_ld);
+      load_chunk(0);
     }
-    // lane b stores batch row b of both positions
-    float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = warp_sum(acc[b]);
+    float v = 0.f;  // lane b stores batch row b
 #pragma unroll
     for (int b = 0; b < NB; ++b)
-      if (lane == b) { v0 = acc0[b]; v1 = acc1[b]; }
+      if (lane == b) v = acc[b];
     if (lane < N) {
-      const float b0 = bias ? __ldg(bias + id0) : 0.f, b1 = bias ? __ldg(bias + id1) : 0.f;
-      v0 += b0;
-      v1 += b1;
-      if (act == PS_ACT_RELU) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
-      const size_t o = (size_t)lane * out_ld + p0;
-      if (out_bf16) {
-        reinterpret_cast<uint16_t*>(out)[o] = f2bf(v0);
-        if (two) reinterpret_cast<uint16_t*>(out)[o + 1] = f2bf(v1);
-      } else {
-        reinterpret_cast<float*>(out)[o] = v0;
-        if (two) reinterpret_cast<float*>(out)[o + 1] = v1;
-      }
+      v += bias ? __ldg(bias + id_done) : 0.f;
+      if (act == PS_ACT_RELU) v = fmaxf(v, 0.f);
+      const size_t o = (size_t)lane * out_ld + p_done;
+      if (out_bf16) reinterpret_cast<uint16_t*>(out)[o] = f2bf(v);
+      else reinterpret_cast<float*>(out)[o] = v;
     }
   }
   // zero the padding positions the next kernel may read
@@ -922,14 +922,21 @@ int launch_gemv_up(const void* w, int64_t w_ld, const int32_t* idx, const int32_
                    cudaStream_t st) {
   const size_t smem = (size_t)NB * K * 2;
   static bool configured = false;
+  static int occ_k = -1, occ = 1;
   if (!configured) {
     if (cudaFuncSetAttribute(gemv_up_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
         cudaSuccess)
       return PS_ERR_CUDA;
     configured = true;
   }
-  const int per_sm = smem <= 100 * 1024 ? 2 : 1;
-  return launch_ex(gemv_up_kernel<NB>, dim3(ps_num_sms() * per_sm), dim3(kGvThreads), smem, st, 1,
+  if (occ_k != K) {  // resident CTAs per SM at this x footprint (registers bound it at small K)
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gemv_up_kernel<NB>, kGvThreads, smem) != cudaSuccess)
+      return PS_ERR_CUDA;
+    occ = n < 1 ? 1 : n;
+    occ_k = K;
+  }
+  return launch_ex(gemv_up_kernel<NB>, dim3(ps_num_sms() * occ), dim3(kGvThreads), smem, st, 1,
                    static_cast<const uint16_t*>(w), w_ld, idx, count_dev, M, static_cast<const uint16_t*>(x), x_ld,
                    N, K, bias, act, out, out_ld, out_bf16, BM);
 }

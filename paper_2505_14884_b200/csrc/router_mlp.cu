@@ -19,7 +19,7 @@
 //   * second grid barrier, then phase 2: the TMA producer streams hid (the B
 //     operand, from L2) behind the prefetched W_out stages and the rest of
 //     W_out; the epilogue writes logits (+ b_out) straight from TMEM.
-// The grid barrier is a self-resetting {generation, count} word.
+// The grid barrier is a monotonic 64-bit counter (grid_arrive / grid_wait).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -36,10 +36,10 @@ constexpr int kRA1 = 4;       // phase-1 A K-blocks per CTA (64 KB)
 constexpr int kRStages = 12;  // phase-2 pipeline stages (at most: as many as the shared memory holds)
 
 struct GridBar {
-  unsigned int count;
-  unsigned int pad[31];
-  unsigned int gen;
+  unsigned long long count;  // monotonic: every barrier adds exactly kBarUnit
+  unsigned long long pad[15];
 };
+constexpr unsigned long long kBarUnit = 1ull << 20;  // > any grid size
 
 struct RParams {
   int B, NB, d, r, D;
@@ -65,32 +65,31 @@ PS_DEV unsigned long long r_time() {
 
 PS_DEV void fence_proxy_async_global_r() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// Grid barrier (one thread per CTA): an arrival counter and, on another
-// 128-byte line, the generation flag the waiters poll (with back-off, so the
-// arrivals do not queue behind the polls).  The last arriver re-zeroes the
-// counter, then releases generation `target`.
+// Grid barrier (one thread per CTA) on a monotonic 64-bit counter: CTA 0
+// adds kBarUnit - (n - 1), every other CTA adds 1, so each barrier advances
+// it by exactly kBarUnit whatever the grid size, and barrier k of a launch
+// whose counter started at `base` has completed once count >= base + k *
+// kBarUnit.  Arrival is a fire-and-forget release reduction and the waiters
+// poll the counter itself: no last-arriver atomic round trip, reset store or
+// second release on the critical path (2.4 / 1.8 -> 1.8 / 1.0 us, B = 1).
+// `base` = count rounded down to a kBarUnit multiple, read before the CTA's
+// first arrival: until barrier 1 completes the partial sums stay below it.
 
-PS_DEV unsigned int ld_acquire_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+PS_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
-PS_DEV void grid_wait_gen(const GridBar* bar, uint32_t target) {
-  while (ld_acquire_u32(&bar->gen) - target > 0x7fffffffu) __nanosleep(20);
+PS_DEV void grid_wait(const GridBar* bar, unsigned long long target) {
+  while (ld_acquire_u64(&bar->count) < target) __nanosleep(20);
 }
 
-// Called by one thread after a CTA barrier: its acq_rel fence is cumulative
-// over the writes the barrier ordered before it (as in a cooperative grid sync).
-PS_DEV void grid_arrive_wait(GridBar* bar, uint32_t target, int nctas) {
-  unsigned int old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(&bar->count) : "memory");
-  if (old == (unsigned int)nctas - 1u) {
-    bar->count = 0u;
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&bar->gen), "r"(target) : "memory");
-  } else {
-    grid_wait_gen(bar, target);
-  }
+// Called by one thread after a CTA barrier: the release is cumulative over
+// the writes the barrier ordered before it (as in a cooperative grid sync).
+PS_DEV void grid_arrive(GridBar* bar, int cta, int nctas) {
+  const unsigned long long add = cta == 0 ? kBarUnit - (unsigned long long)(nctas - 1) : 1ull;
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(add) : "memory");
 }
 
 __global__ void __launch_bounds__(kRThreads, 1)
@@ -117,7 +116,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
   uint64_t* genbar = p2done + 1;  // the producer read this launch's barrier generation
   uint64_t* xfull = genbar + 1;   // [kRA1] phase-2 K-blocks S2 .. S2+3 in the phase-1 buffers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + kRA1);
-  uint32_t& s_gen0 = tmem_slot[1];
+  unsigned long long& s_base = reinterpret_cast<unsigned long long*>(tmem_slot)[1];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cta = blockIdx.x, nctas = gridDim.x;
@@ -175,12 +174,12 @@ __global__ void __launch_bounds__(kRThreads, 1)
       }
       if (tr) tr[1] = r_time();
       griddep_wait();  // h comes from the previous kernel
-      // generation of this launch: read after the previous grid (possibly the
-      // previous launch of this kernel on the same workspace) completed; it
-      // cannot advance before this CTA arrives
-      const uint32_t gen0 = ld_acquire_u32(&p.bar->gen);
+      // barrier base of this launch: read after the previous grid (possibly the
+      // previous launch of this kernel on the same workspace) completed, and
+      // before this CTA arrives (so barrier 1 cannot have completed)
+      const unsigned long long base = ld_acquire_u64(&p.bar->count) / kBarUnit * kBarUnit;
       if (tr) tr[7] = r_time();
-      s_gen0 = gen0;
+      s_base = base;
       mbar_arrive(genbar);
       if (has1) {
         mbar_arrive_expect_tx(b1full, (uint32_t)n1 * b_bytes);
@@ -195,7 +194,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
         tma_load_2d(A1 + i * a_bytes, &tmWout, (S2 + i) * RBK, t2 * RBM, &xfull[i]);
       }
       // ---- phase 2: hid is complete after the second grid barrier
-      grid_wait_gen(p.bar, gen0 + 2u);
+      grid_wait(p.bar, base + 2 * kBarUnit);
       if (tr) tr[4] = r_time();
       for (int kb = 0; kb < kb2; ++kb) {
         if (kb >= S2 && kb < S2 + nx) {  // a phase-1 buffer, used once
@@ -286,12 +285,13 @@ __global__ void __launch_bounds__(kRThreads, 1)
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kREpi));
-    uint32_t gen0 = 0;
+    unsigned long long base = 0;
     if (et == 0) {
       if (tr) tr[2] = r_time();
       mbar_wait(genbar, 0);
-      gen0 = s_gen0;
-      grid_arrive_wait(p.bar, gen0 + 1u, nctas);
+      base = s_base;
+      grid_arrive(p.bar, cta, nctas);
+      grid_wait(p.bar, base + kBarUnit);
       if (tr) tr[3] = r_time();
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kREpi));
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
     fence_proxy_async_global_r();  // generic hid stores -> the other CTAs' TMA (async proxy) loads
     if (tr && et == 0) tr[11] = r_time();
     asm volatile("bar.sync 1, %0;" ::"n"(kREpi));
-    if (et == 0) grid_arrive_wait(p.bar, gen0 + 2u, nctas);
+    if (et == 0) grid_arrive(p.bar, cta, nctas);
     // phase 2: logits tile straight from TMEM (lanes = consecutive logit columns)
     mbar_wait(p2done, 0);
     tc_fence_after();

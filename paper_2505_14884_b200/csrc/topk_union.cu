@@ -348,14 +348,17 @@ __global__ void __launch_bounds__(kTuThreads, 1) topk_union_kernel(const TuParam
     p.trace[row * 16 + 9] = clock64();
   }
   // ---- the last row CTA compacts
+  // one acq_rel ticket (release: this CTA's bitmap ORs, ordered before it by
+  // the barrier; acquire: every other CTA's, for the compacting CTA) instead
+  // of a fence on each side of a relaxed atomic
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(p.ticket, 1) == p.rows - 1;
+    unsigned int old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.ticket) : "memory");
+    s_last = old == (unsigned int)p.rows - 1u;
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   if (p.trace && tid == 0) p.trace[row * 16 + 6] = tu_time();
   const int words = (cols + 31) >> 5;
   const int wlo = p.lo >> 5, whi = (p.hi + 31) >> 5;

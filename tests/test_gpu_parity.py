@@ -499,15 +499,17 @@ def test_kv_append_and_capacity():
         c.append_step(k, v)
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 4])
-def test_small_batch_gemv_up_matches_tiles_and_torch(N):
+@pytest.mark.parametrize("N,d,D", [(1, 4096, 16384), (2, 4096, 16384), (3, 4096, 16384), (4, 4096, 16384),
+                                   (1, 9216, 12288), (4, 2560, 10240)])
+def test_small_batch_gemv_up_matches_tiles_and_torch(N, d, D):
     """N <= 4: the UP projection runs on the gathered GEMV (whole rows per
     warp); it matches the tcgen05 tile path and an fp32 torch reference, and
-    zeroes the padding positions the DOWN projection may read."""
+    zeroes the padding positions the DOWN projection may read.  d = 9216
+    streams each row in 8 KB chunks with a partial last chunk; d = 2560 is a
+    single partial chunk."""
     from paper_2505_14884_b200 import _lib, kernels as pk
 
     gen = torch.Generator(device=DEV).manual_seed(N)
-    d, D = 4096, 16384
     w1t = (torch.randn(D, d, device=DEV, generator=gen) * 0.02).bfloat16()
     b1 = torch.randn(D, device=DEV, generator=gen) * 0.02
     x = torch.randn(N, d, device=DEV, generator=gen).bfloat16()
@@ -521,7 +523,7 @@ def test_small_batch_gemv_up_matches_tiles_and_torch(N):
     for gemv in (1, 0):
         L.ps_debug_gemm_gemv(gemv)
         try:
-            out = torch.full((N, 16384 + 128), float("nan"), device=DEV).bfloat16()
+            out = torch.full((N, D + 128), float("nan"), device=DEV).bfloat16()
             pk.gather_gemm_into(w1t, nit.buffer, nit.count, x, d, b1, N, D, d, _lib.PS_ACT_RELU, out, out.stride(0),
                                 splits=count)
             torch.cuda.synchronize()
