@@ -93,8 +93,9 @@ def parse(argv=None):
                     help="paged KV caches with this many rows per page (0 = contiguous)")
     ap.add_argument("--kv-reserve", default="full", choices=["full", "on_demand"],
                     help="paged KV: map every page up front, or each page as the appends enter it")
-    ap.add_argument("--concurrent-head-router", action="store_true",
-                    help="head router as a concurrent graph branch instead of fused with the KV append")
+    ap.add_argument("--concurrent-head-router", choices=("auto", "on", "off"), default="auto", nargs="?",
+                    const="on", help="head router as a concurrent graph branch (+ a separate KV append) instead of "
+                    "fused with the KV append; auto = on for B <= 8 without TP (the engine default)")
     return ap.parse_args(argv)
 
 
@@ -447,7 +448,8 @@ class Setup:
         polar = SparsityPolicy(mode="polar", head_density=args.rho,
                                mlp_k_table={ell: k for ell in range(L)} if self.relu else None)
         self.eng = DecodeEngine(self.model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=self.ring,
-                                router_backend=args.router_backend, concurrent_router=args.concurrent_head_router,
+                                router_backend=args.router_backend,
+                                concurrent_router={"on": True, "off": False}.get(args.concurrent_head_router),
                                 tp=self.tp, kv_page_rows=args.kv_page_rows, kv_reserve=args.kv_reserve)
         self.eng.fill_random(ctx, seed=99 + (0 if tp_on else rank))
         self.dense = DecodeEngine(self.model, B, cap, SparsityPolicy(mode="dense"), caches=self.eng.caches,
@@ -681,7 +683,9 @@ def run_ours(args):
     main_ideal = ideal_ratio(cfg, B, args.ctx, args.rho, S_meas)
     setup_info = {"kv_storage_buffers": su.ring, "graph_captured": su.graphs, "graph_error": su.graph_error,
                   "kv_aliasing": ("none" if su.ring == L else f"K/V storage aliased over {su.ring} buffers"),
-                  "hot_set": su.n_hot, "k_per_token": su.k_mlp}
+                  "hot_set": su.n_hot, "k_per_token": su.k_mlp,
+                  "head_router": "concurrent branch" if su.eng.concurrent_router else "fused with the KV append",
+                  "mlp_router": su.eng.router_backend}
     del su, eng, dense, sha_graph
     torch.cuda.empty_cache()
 

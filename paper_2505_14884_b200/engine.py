@@ -88,7 +88,7 @@ class DecodeEngine:
     def __init__(self, model: DeviceModel, batch: int, capacity: int, policy: SparsityPolicy,
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
                  caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
-                 concurrent_router: bool = False, kv_page_rows: int = 0, kv_reserve: str = "full",
+                 concurrent_router: bool | None = None, kv_page_rows: int = 0, kv_reserve: str = "full",
                  mlp_backend: str = "split"):
         cfg = model.config
         check_count(batch, "batch")
@@ -106,13 +106,19 @@ class DecodeEngine:
         self.router_backend = check_choice(router_backend or dense_backend,
                                            ("fused", "cublas", "native", "native_in"), "router_backend")
         # head router on a side stream, concurrent with the QKV GEMM (a
-        # parallel branch of the captured graph); False = fused with the append
-        self.concurrent_router = concurrent_router
+        # parallel branch of the captured graph) + a separate KV append; False
+        # = fused with the append after the QKV GEMM.  Default: concurrent for
+        # B <= 8 without TP (OPT-6.7B per step, same box: B=1 3.478 -> 3.341 ms,
+        # B=2 3.548 -> 3.438, B=4 3.819 -> 3.714, B=8 4.302 -> 4.190; B=16
+        # 5.052 -> 5.138 and B=64 slower: the cluster competes with the GEMM)
+        if concurrent_router is None:
+            concurrent_router = batch <= 8 and tp is None
+        self.concurrent_router = bool(concurrent_router)
         # selective MLP: "split" = UP and DOWN as two tcgen05 launches
         # (ps_gather_gemm / _t); "chain" = both in one persistent launch
         # (ps_sparse_mlp, batch <= 256)
         self.mlp_backend = check_choice(mlp_backend, ("split", "chain"), "mlp_backend")
-        self.side = torch.cuda.Stream(device=model.device) if concurrent_router else None
+        self.side = torch.cuda.Stream(device=model.device) if self.concurrent_router else None
         self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
         self.tp = tp
