@@ -685,7 +685,7 @@ def run_ours(args):
                   "kv_aliasing": ("none" if su.ring == L else f"K/V storage aliased over {su.ring} buffers"),
                   "hot_set": su.n_hot, "k_per_token": su.k_mlp,
                   "head_router": "concurrent branch" if su.eng.concurrent_router else "fused with the KV append",
-                  "mlp_router": su.eng.router_backend}
+                  "mlp_router": su.eng.router_backend, "o_proj": su.eng.o_backend}
     del su, eng, dense, sha_graph
     torch.cuda.empty_cache()
 

@@ -89,7 +89,7 @@ class DecodeEngine:
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
                  caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
                  concurrent_router: bool | None = None, kv_page_rows: int = 0, kv_reserve: str = "full",
-                 mlp_backend: str = "split"):
+                 mlp_backend: str = "split", o_backend: str | None = None):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
@@ -118,6 +118,14 @@ class DecodeEngine:
         # (ps_gather_gemm / _t); "chain" = both in one persistent launch
         # (ps_sparse_mlp, batch <= 256)
         self.mlp_backend = check_choice(mlp_backend, ("split", "chain"), "mlp_backend")
+        # attention output projection (+ residual): cuBLAS, or the tcgen05
+        # dense kernel, whose static W_o streams ahead of the SHA tail (PDL) and
+        # which hands LayerNorm a PDL edge.  Default: native for B <= 8 without
+        # TP (OPT-6.7B per step, same box: B=1 3.347 -> 3.301 ms, B=4 3.745 ->
+        # 3.67-3.72, B=8 4.192 -> 4.167; B=16 5.059 -> 5.14, B=64 +0.8 %)
+        if o_backend is None:
+            o_backend = "native" if batch <= 8 and tp is None else dense_backend
+        self.o_backend = check_choice(o_backend, ("cublas", "native"), "o_backend")
         self.side = torch.cuda.Stream(device=model.device) if self.concurrent_router else None
         self._cache = {}
         self.head_routers, self.mlp_routers = head_routers, mlp_routers
@@ -312,7 +320,7 @@ class DecodeEngine:
         the residual in its epilogue (beta = 1).  With ``defer_bias`` the
         bias is NOT added here: the caller hands it to the next
         ps_add_layernorm as the pending bias (returned as the 2nd value)."""
-        if self.dense_backend == "cublas":
+        if self.dense_backend == "cublas" and not (tag == "gg_o" and self.o_backend == "native"):
             if residual:
                 torch.addmm(out, x2d, w_t.t(), out_dtype=torch.float32, out=out)
             elif bias is not None and not defer_bias:  # bias in the GEMM epilogue
