@@ -93,6 +93,9 @@ def parse(argv=None):
                     help="paged KV caches with this many rows per page (0 = contiguous)")
     ap.add_argument("--kv-reserve", default="full", choices=["full", "on_demand"],
                     help="paged KV: map every page up front, or each page as the appends enter it")
+    ap.add_argument("--union-handoff", choices=("auto", "on", "off"), default="auto",
+                    help="selection writes only the union bitmap and UP / DOWN derive the ids on the device "
+                    "(auto = the engine default: off)")
     ap.add_argument("--concurrent-head-router", choices=("auto", "on", "off"), default="auto", nargs="?",
                     const="on", help="head router as a concurrent graph branch (+ a separate KV append) instead of "
                     "fused with the KV append; auto = on for B <= 8 without TP (the engine default)")
@@ -450,6 +453,7 @@ class Setup:
         self.eng = DecodeEngine(self.model, B, cap, polar, head_routers=hr, mlp_routers=mr, kv_ring=self.ring,
                                 router_backend=args.router_backend,
                                 concurrent_router={"on": True, "off": False}.get(args.concurrent_head_router),
+                                union_handoff={"on": True, "off": False}.get(args.union_handoff),
                                 tp=self.tp, kv_page_rows=args.kv_page_rows, kv_reserve=args.kv_reserve)
         self.eng.fill_random(ctx, seed=99 + (0 if tp_on else rank))
         self.dense = DecodeEngine(self.model, B, cap, SparsityPolicy(mode="dense"), caches=self.eng.caches,
@@ -685,7 +689,8 @@ def run_ours(args):
                   "kv_aliasing": ("none" if su.ring == L else f"K/V storage aliased over {su.ring} buffers"),
                   "hot_set": su.n_hot, "k_per_token": su.k_mlp,
                   "head_router": "concurrent branch" if su.eng.concurrent_router else "fused with the KV append",
-                  "mlp_router": su.eng.router_backend, "o_proj": su.eng.o_backend}
+                  "mlp_router": su.eng.router_backend, "o_proj": su.eng.o_backend,
+                  "union_handoff": su.eng.union_handoff}
     del su, eng, dense, sha_graph
     torch.cuda.empty_cache()
 

@@ -161,6 +161,14 @@ size_t ps_select_union_workspace_bytes(int rows, int cols);
 int ps_select_union(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k, float thr,
                     void* ws, size_t ws_bytes, int lo, int hi, int pad,
                     int32_t* union_out, int32_t* count_out, void* stream);
+/* ps_select_union_bitmap -- union hand-off: the per-row top-k (k >= 1) or
+ * threshold (k <= 0: logit > thr) sets are OR-ed into `bitmap` (ceil(cols/32)
+ * uint32 words, zero on entry) and the launch ends there: no ticket, no
+ * compaction.  The gathered GEMMs read the bitmap (PS_GG_BITMAP).  CTA 0
+ * zeroes `clear` (the buffer of the previous layer; may be NULL), so two
+ * buffers alternate layer by layer.  cols <= 36864. */
+int ps_select_union_bitmap(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k, float thr,
+                           uint32_t* bitmap, uint32_t* clear, void* stream);
 /* debug: per-CTA phase timestamps of the top-k kernel (16 x u64 per CTA), NULL = off */
 void ps_debug_topk_trace(void* buf);
 /* ps_select_union kernel: 1 = the low-latency row kernel (topk_union.cu,
@@ -241,6 +249,13 @@ void ps_debug_gemm_gemv(int enable);
  * launch).  Without it (or with idx == count_dev == NULL, i.e. static dense
  * weights, where it is implied) only static data is read early. */
 #define PS_GG_A_READY 1
+/* flags: PS_GG_BITMAP -- union hand-off: `idx` is the union BITMAP over the
+ * w_height weight rows (ceil(w_height / 32) uint32 words, as written by
+ * ps_select_union_bitmap) instead of a compacted id list; the kernel derives
+ * the ids on the device (word-prefix popcounts).  UP writes the union size to
+ * count_dev (may be NULL); DOWN ignores count_dev.  Tensor-core path only
+ * (not the N <= 4 GEMV); w_height <= 32768. */
+#define PS_GG_BITMAP 2
 size_t ps_gather_gemm_workspace_bytes(int N, int M, int K, int splits);
 int ps_gather_gemm_auto_splits(int N, int M, int K);
 int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,

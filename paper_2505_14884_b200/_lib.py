@@ -22,6 +22,7 @@ PS_DTYPE_BF16 = 1
 PS_ACT_NONE = 0
 PS_ACT_RELU = 1
 PS_GG_A_READY = 1
+PS_GG_BITMAP = 2
 
 _vp = ctypes.c_void_p
 _i = ctypes.c_int
@@ -48,6 +49,7 @@ SIGNATURES = {
     "ps_threshold_rows": (_i, [_vp, _i, _i, _i64, _f, _vp, _vp]),
     "ps_select_union_workspace_bytes": (_sz, [_i, _i]),
     "ps_select_union": (_i, [_vp, _vp, _i, _i, _i64, _i, _f, _vp, _sz, _i, _i, _i, _vp, _vp, _vp]),
+    "ps_select_union_bitmap": (_i, [_vp, _vp, _i, _i, _i64, _i, _f, _vp, _vp, _vp]),
     "ps_union_rows": (_i, [_vp, _i, _i, _i, _vp, _vp]),
     "ps_bitmap_compact": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp]),
     "ps_head_router_topk": (_i, [_vp, _i64, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp]),

@@ -72,6 +72,12 @@ struct GGParams {
   int vec_ok;  // out / residual rows 16-byte aligned: vector epilogue stores
   int push;     // split-K reduction: 1 = partial rows pushed to their owner CTA (st.async), 0 = pulled (DSMEM loads)
   int a_early;  // A (weights, idx, count) ready before the previous kernel ends: stream A pre-griddep_wait
+  // union hand-off (PS_GG_BITMAP): the ids are derived on the device from the
+  // selection bitmap (bm_words uint32 words) instead of a compacted id list
+  const uint32_t* bm;
+  int bm_words;
+  int32_t* count_out;  // UP, bitmap mode: receives the union size
+  int ids_cap;         // bitmap mode: ids expanded into shared memory up front (the rest: cursor walk)
   unsigned long long* trace;  // debug: per-CTA timestamps (ps_debug_gemm_trace), NULL normally
 };
 
@@ -146,6 +152,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* fre = rdy + 1;       // cluster: every CTA done reading the staged tiles
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fre + 1);
   float* stg = reinterpret_cast<float*>(smem + S * stage_bytes + 256);  // [kEpiCols][BM] f32
+  uint32_t* s_bw = reinterpret_cast<uint32_t*>(stg + kEpiCols * BM);  // bitmap mode: [bm_words] words
+  int* s_bpre = reinterpret_cast<int*>(s_bw + p.bm_words);            // [bm_words + 1] prefix popcounts
+  int* s_bscan = s_bpre + p.bm_words + 1;                              // [kThreads / 32] warp totals
+  uint16_t* s_ids = reinterpret_cast<uint16_t*>(s_bscan + kThreads / 32);  // [ids_cap] ids of this CTA's positions
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = (int)cluster_size();
@@ -200,8 +210,65 @@ __global__ void __launch_bounds__(kThreads, 2)
     griddep_wait();
     if (tid == 0) griddep_launch();
   }
+  // ---- union hand-off: word-prefix popcounts of the selection bitmap, so
+  // union position `pos` maps to its id with a binary search + __fns (no
+  // compacted id list, no compaction on the selection kernel's tail)
+  if (GATHER && p.bm) {
+    const int nw = p.bm_words;
+    const int per = (nw + kThreads - 1) / kThreads;
+    const int w0 = tid * per;
+    int loc = 0;
+    for (int q = 0; q < per; ++q) {
+      const int w = w0 + q;
+      if (w < nw) {
+        const uint32_t a = __ldcg(p.bm + w);
+        s_bw[w] = a;
+        loc += __popc(a);
+      }
+    }
+    int incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_bscan[warp] = incl;
+    __syncthreads();
+    int run = incl - loc;
+    for (int i = 0; i < warp; ++i) run += s_bscan[i];
+    for (int q = 0; q < per; ++q) {
+      const int w = w0 + q;
+      if (w < nw) {
+        s_bpre[w] = run;
+        run += __popc(s_bw[w]);
+      }
+    }
+    if (tid == 0) {
+      int tot = 0;
+      for (int i = 0; i < kThreads / 32; ++i) tot += s_bscan[i];
+      s_bpre[nw] = tot;
+    }
+    __syncthreads();
+  }
+  // bitmap mode: the word holding union position pos (< count) by binary
+  // search, then ascending positions walk forward from it (a thread's
+  // positions are increasing, a few words apart)
+  auto bm_seek = [&](int pos) -> int {
+    int lo = 0, hi = p.bm_words - 1;  // the last word whose prefix is <= pos holds it
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_bpre[mid] <= pos) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+  auto bm_id = [&](int pos, int& w) -> int {  // w: a word at or before pos's word
+    while (s_bpre[w + 1] <= pos) ++w;
+    return w * 32 + (int)__fns(s_bw[w], 0u, pos - s_bpre[w] + 1);
+  };
   // ---- device-side work partition (identical in every role and CTA of a cluster)
-  const int count = p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K);
+  const int count = (GATHER && p.bm) ? s_bpre[p.bm_words] : (p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K));
+  if (MODE == MODE_UP && GATHER && p.bm && p.count_out && blockIdx.x == 0 && tid == 0) *p.count_out = count;
   const int klimit = (MODE == MODE_UP) ? p.K : count;
   const int kbt = (klimit + BK - 1) / BK;
   const int live_m = (MODE == MODE_UP) ? (count + BM - 1) / BM : (p.M + BM - 1) / BM;
@@ -210,6 +277,35 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int kb0 = rank * per;
   const int nkb = max(0, min(kbt, kb0 + per) - kb0);  // K blocks of this CTA (same for every tile)
   const int my_tiles = cid < tiles ? (tiles - cid + ncl - 1) / ncl : 0;
+  // bitmap mode: expand the ids of this CTA's union positions (DOWN: its K
+  // range; UP: its first tile) into shared memory with every thread, one word
+  // each, so the loaders read them with one shared load
+  int ids_p0 = 0, ids_n = 0;
+  if (GATHER && p.bm) {
+    if (MODE == MODE_DOWN) {
+      ids_p0 = kb0 * BK;
+      ids_n = min(count, (kb0 + nkb) * BK) - ids_p0;
+    } else {
+      ids_p0 = live_m > 0 ? (cid % live_m) * BM : 0;
+      ids_n = min(count, ids_p0 + BM) - ids_p0;
+    }
+    if (my_tiles == 0 || ids_n < 0) ids_n = 0;
+    if (ids_n > p.ids_cap) ids_n = p.ids_cap;
+    if (ids_n > 0) {
+      const int wa = bm_seek(ids_p0), wb = bm_seek(ids_p0 + ids_n - 1);
+      for (int w = wa + tid; w <= wb; w += kThreads) {
+        uint32_t bits = s_bw[w];
+        int q = s_bpre[w] - ids_p0;
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (q >= 0 && q < ids_n) s_ids[q] = (uint16_t)(w * 32 + b);
+          ++q;
+        }
+      }
+    }
+    __syncthreads();
+  }
   // every CTA of a cluster sees the same my_tiles, so whole clusters leave together
   if (my_tiles == 0) {
     if (p.a_early) {
@@ -287,19 +383,29 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int m0 = (t % live_m) * BM;
         const uint16_t* src[8];  // UP: this thread's 8 rows of the tile
         if (MODE == MODE_UP) {
+          int bw = (GATHER && p.bm && j > 0 && m0 + (lt >> 3) < count) ? bm_seek(m0 + (lt >> 3)) : 0;
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const int gr = m0 + (lt >> 3) + 16 * r;
-            const int id = gr < count ? (GATHER ? __ldg(p.idx + gr) : gr) : -1;
+            const int id = gr < count ? (GATHER ? (p.bm ? (j == 0 && gr - ids_p0 < ids_n ? (int)s_ids[gr - ids_p0]
+                                                                                         : bm_id(gr, bw))
+                                                            : __ldg(p.idx + gr))
+                                                : gr)
+                                      : -1;
             src[r] = id >= 0 ? p.w + (size_t)id * p.w_ld + (lt & 7) * 8 : nullptr;
           }
         }
         int kid[8];  // DOWN: ids of this thread's 8 K rows of the current stage (prefetched)
+        int dw = -1;   // bitmap mode: word cursor (positions ascend through the tile's K blocks)
         auto down_ids = [&](int kb, int* o) {
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const int kg = kb * BK + (lt >> 4) + 8 * r;
-            o[r] = kg < count ? (GATHER ? __ldg(p.idx + kg) : kg) : -1;
+            if (GATHER && p.bm && kg < count && kg - ids_p0 >= ids_n && dw < 0) dw = bm_seek(kg);
+            o[r] = kg < count ? (GATHER ? (p.bm ? (kg - ids_p0 < ids_n ? (int)s_ids[kg - ids_p0] : bm_id(kg, dw))
+                                                : __ldg(p.idx + kg))
+                                       : kg)
+                              : -1;
           }
         };
         if (MODE == MODE_DOWN && nkb > 0) down_ids(kb0, kid);
@@ -409,12 +515,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int nrows = min(NB, p.N - n0);
       float my_bias[4] = {0.f, 0.f, 0.f, 0.f};
       bool my_live[4];
+      int ew = (MODE == MODE_UP && GATHER && p.bm && p.bias && j > 0 && m0 + my_m < count) ? bm_seek(m0 + my_m) : 0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int gm = m0 + my_m + u;
         my_live[u] = (MODE == MODE_UP) ? gm < count : gm < p.M;
         if (my_live[u] && p.bias)
-          my_bias[u] = __ldg(p.bias + ((MODE == MODE_UP && p.idx) ? __ldg(p.idx + gm) : gm));
+          my_bias[u] = __ldg(p.bias + ((MODE == MODE_UP && p.idx)
+                                           ? (p.bm ? (j == 0 && gm - ids_p0 < ids_n ? (int)s_ids[gm - ids_p0]
+                                                                                    : bm_id(gm, ew))
+                                                   : __ldg(p.idx + gm))
+                                           : gm));
       }
       auto load_res = [&](int n) -> float4 {
         float res[4] = {0.f, 0.f, 0.f, 0.f};
@@ -714,7 +825,9 @@ int make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uin
 template <int MODE, bool GATHER, bool LSU_A>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GGParams& prm, int cluster, int work_ctas,
              cudaStream_t st) {
-  const size_t smem = smem_bytes(prm.NB, prm.stages);
+  const size_t smem = smem_bytes(prm.NB, prm.stages) +
+                      (prm.bm ? 4 * (2 * (size_t)prm.bm_words + 1 + kThreads / 32) + ((size_t)prm.ids_cap * 2 + 15) / 16 * 16
+                              : 0);
   auto kern = gather_gemm_kernel<MODE, GATHER, LSU_A>;
   static bool configured = false;
   if (!configured) {
@@ -747,6 +860,8 @@ int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, int tile
   if (rc != PS_OK) return rc;
   const int cluster = pick_cluster(prm.NB, tiles_est * prm.n_tiles, kbt_est);
   const int work = tiles_est * prm.n_tiles * cluster;
+  // bitmap mode: ids expanded up front (one more K block of margin for DOWN)
+  prm.ids_cap = MODE == MODE_DOWN ? ((kbt_est + cluster - 1) / cluster + 1) * BK : BM;
   const bool lsu = g_lsu_mode == 2 || (g_lsu_mode == 1 && gather);
   if (gather)
     return lsu ? launch_t<MODE, true, true>(ta, tb, prm, cluster, work, st)
@@ -782,6 +897,10 @@ static int gg_common(GGParams& prm, const void* w_rows, const int32_t* idx, cons
   prm.w = static_cast<const uint16_t*>(w_rows);
   prm.idx = idx;
   prm.count = count_dev;
+  prm.bm = nullptr;
+  prm.bm_words = 0;
+  prm.count_out = nullptr;
+  prm.ids_cap = 0;
   prm.x = static_cast<const uint16_t*>(x);
   prm.x_ld = x_ld;
   prm.bias = bias;
@@ -944,6 +1063,21 @@ int launch_gemv_up(const void* w, int64_t w_ld, const int32_t* idx, const int32_
 }  // namespace
 }  // namespace ps
 
+// PS_GG_BITMAP: `idx` is the union bitmap over the w_height weight rows
+// (ceil(w_height / 32) uint32 words); the tcgen05 path with the cp.async A
+// loaders derives the ids from it on the device.  UP writes the union size to
+// count_dev (may be NULL); DOWN ignores count_dev.
+static int gg_bitmap(GGParams& prm, const int32_t* idx, int32_t* count_out, int w_height, int rows_max) {
+  if (!idx || g_lsu_mode < 1) return PS_ERR_UNSUPPORTED;
+  const int words = (w_height + 31) / 32;
+  if ((int64_t)words * 32 > (int64_t)rows_max + 31 || words > 1024) return PS_ERR_VALUE;
+  prm.bm = reinterpret_cast<const uint32_t*>(idx);
+  prm.bm_words = words;
+  prm.count = nullptr;
+  prm.count_out = count_out;
+  return PS_OK;
+}
+
 extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* idx, const int32_t* count_dev,
                               const void* x, int64_t x_ld, const float* bias, const float* residual,
                               int64_t residual_ld, int N, int M, int K, int act, int splits, int flags, void* out,
@@ -960,6 +1094,13 @@ extern "C" int ps_gather_gemm(const void* w_rows, int w_height, const int32_t* i
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;
   if (w_height < (idx ? 1 : M)) return PS_ERR_VALUE;
+  if (flags & PS_GG_BITMAP) {
+    const int st2 = gg_bitmap(prm, idx, const_cast<int32_t*>(count_dev), w_height, M);
+    if (st2 != PS_OK) return st2;
+    const int rows_est = splits > 0 ? (splits < M ? splits : M) : M;
+    return launch<MODE_UP>(prm, w_height, K, K, (rows_est + BM - 1) / BM, (K + BK - 1) / BK,
+                           static_cast<cudaStream_t>(stream));
+  }
   if (g_gemv < 0) {
     const char* e = getenv("PS_GG_GEMV");
     g_gemv = e ? atoi(e) : 1;
@@ -992,6 +1133,10 @@ extern "C" int ps_gather_gemm_t(const void* w_rows, int w_height, const int32_t*
   prm.res_ld = residual_ld;
   if (residual && ((residual_ld % 4) || ((uintptr_t)residual % 16))) prm.vec_ok = 0;
   if (w_height < (idx ? 1 : K_max)) return PS_ERR_VALUE;
+  if (flags & PS_GG_BITMAP) {
+    const int st2 = gg_bitmap(prm, idx, nullptr, w_height, K_max);
+    if (st2 != PS_OK) return st2;
+  }
   // the K extent (union size) is read on the device; `splits` > 0 is its expected value
   const int k_est = splits > 0 ? (splits < K_max ? splits : K_max) : K_max;
   return launch<MODE_DOWN>(prm, w_height, M, K_max, (M + BM - 1) / BM, (k_est + BK - 1) / BK,

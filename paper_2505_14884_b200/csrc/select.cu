@@ -1164,6 +1164,8 @@ int select_union_v2(const float* logits, const float* bias, int rows, int cols, 
                     int* ticket, uint32_t* bitmap, int lo, int hi, int pad, int32_t* union_out, int32_t* count_out,
                     unsigned long long* trace, cudaStream_t st);
 int select_union_v2_max_cols();
+int select_union_v2_bitmap(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k, float thr,
+                           uint32_t* bitmap, uint32_t* clear, unsigned long long* trace, cudaStream_t st);
 }  // namespace ps
 static int g_topk_v2 = -1;  // -1: from env PS_TOPK_V2 (default 1)
 static const int g_topk_coop = [] {
@@ -1208,6 +1210,18 @@ extern "C" int ps_select_union(const float* logits, const float* bias, int rows,
   prm.lo = lo; prm.hi = hi; prm.pad = pad;
   prm.union_out = union_out; prm.count_out = count_out;
   return launch_topk(prm, static_cast<cudaStream_t>(stream));
+}
+
+// Union hand-off: the rows' top-k (or threshold) sets OR-ed into `bitmap`
+// (ceil(cols / 32) words, zero on entry) and nothing else -- the gathered
+// GEMMs read the bitmap (PS_GG_BITMAP).  CTA 0 zeroes `clear` (may be NULL),
+// the buffer the previous layer used, so two buffers alternate.
+extern "C" int ps_select_union_bitmap(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k,
+                                      float thr, uint32_t* bitmap, uint32_t* clear, void* stream) {
+  if (rows < 1 || cols < 1 || ld < cols || k > cols || !logits || !bitmap || bitmap == clear) return PS_ERR_VALUE;
+  if (cols > select_union_v2_max_cols()) return PS_ERR_UNSUPPORTED;
+  return select_union_v2_bitmap(logits, bias, rows, cols, ld, k > 0 ? k : 0, thr, bitmap, clear, g_topk_trace,
+                                static_cast<cudaStream_t>(stream));
 }
 
 extern "C" void ps_debug_topk_trace(void* buf) { g_topk_trace = static_cast<unsigned long long*>(buf); }

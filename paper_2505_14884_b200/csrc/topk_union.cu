@@ -51,6 +51,10 @@ struct TuParams {
   int32_t* union_out;
   int32_t* count_out;
   unsigned long long* trace;
+  // union hand-off (ps_select_union_bitmap): rows only OR into `bitmap`; no
+  // ticket, no compaction, no reset; CTA 0 zeroes `clear` (the other buffer)
+  int no_compact;
+  uint32_t* clear;
 };
 
 PS_DEV uint32_t tu_key(float f) {  // order-preserving; 0 = NaN (below -inf)
@@ -130,6 +134,8 @@ __global__ void __launch_bounds__(kTuThreads, 1) topk_union_kernel(const TuParam
   if (tid == 0) s_ncand = 0;
   griddep_wait();
   griddep_launch();
+  if (p.clear && row == 0)  // last read by the previous layer's GEMMs, which completed before this grid
+    for (int w = tid; w < ((cols + 31) >> 5); w += kTuThreads) p.clear[w] = 0u;
   if (p.trace && tid == 0) {
     p.trace[row * 16 + 0] = tu_time();
     p.trace[row * 16 + 8] = clock64();
@@ -347,6 +353,7 @@ __global__ void __launch_bounds__(kTuThreads, 1) topk_union_kernel(const TuParam
     p.trace[row * 16 + 5] = tu_time();
     p.trace[row * 16 + 9] = clock64();
   }
+  if (p.no_compact) return;  // the GEMMs read the bitmap (PS_GG_BITMAP)
   // ---- the last row CTA compacts
   // one acq_rel ticket (release: this CTA's bitmap ORs, ordered before it by
   // the barrier; acquire: every other CTA's, for the compacting CTA) instead
@@ -457,5 +464,22 @@ int select_union_v2(const float* logits, const float* bias, int rows, int cols, 
 }
 
 int select_union_v2_max_cols() { return 9 * kTuChunk; }
+
+int select_union_v2_bitmap(const float* logits, const float* bias, int rows, int cols, int64_t ld, int k, float thr,
+                           uint32_t* bitmap, uint32_t* clear, unsigned long long* trace, cudaStream_t st) {
+  TuParams prm{};
+  prm.logits = logits; prm.rows = rows; prm.cols = cols; prm.ld = ld; prm.k = k; prm.thr = thr;
+  prm.bias = bias; prm.bitmap = bitmap; prm.ticket = nullptr;
+  prm.lo = 0; prm.hi = cols; prm.pad = 1; prm.union_out = nullptr; prm.count_out = nullptr;
+  prm.trace = trace;
+  prm.no_compact = 1;
+  prm.clear = clear;
+  if (cols <= 1 * kTuChunk) return launch_tu<1>(prm, st);
+  if (cols <= 2 * kTuChunk) return launch_tu<2>(prm, st);
+  if (cols <= 4 * kTuChunk) return launch_tu<4>(prm, st);
+  if (cols <= 8 * kTuChunk) return launch_tu<8>(prm, st);
+  if (cols <= 9 * kTuChunk) return launch_tu<9>(prm, st);
+  return PS_ERR_UNSUPPORTED;
+}
 
 }  // namespace ps

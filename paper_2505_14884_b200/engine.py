@@ -27,7 +27,8 @@ import torch
 
 from . import _lib, _ws
 from .exceptions import CapacityError, ConfigurationError
-from .kernels import ROW_PAD, _round_up, gather_gemm_into, mlp_into, sha_decode_into, sparse_mlp_into, swiglu_into
+from .kernels import (ROW_PAD, _round_up, gather_gemm_into, mlp_into, mlp_into_bitmap, sha_decode_into,
+                      sparse_mlp_into, swiglu_into)
 from .model import DeviceModel, TransformerConfig
 from .tensors import KVCache, PagedKVCache
 from .validation import check_choice, check_count
@@ -89,7 +90,7 @@ class DecodeEngine:
                  head_routers=None, mlp_routers=None, kv_ring: int | None = None, tp=None,
                  caches=None, dense_backend: str = "cublas", router_backend: str | None = None,
                  concurrent_router: bool | None = None, kv_page_rows: int = 0, kv_reserve: str = "full",
-                 mlp_backend: str = "split", o_backend: str | None = None):
+                 mlp_backend: str = "split", o_backend: str | None = None, union_handoff: bool | None = None):
         cfg = model.config
         check_count(batch, "batch")
         check_count(capacity, "capacity")
@@ -223,6 +224,26 @@ class DecodeEngine:
             self.union_idx = torch.zeros(_round_up(D, ROW_PAD), dtype=torch.int32, device=dev)
             # per-layer device union sizes (the count each layer's MLP reads)
             self.union_counts = torch.zeros(cfg.layers, dtype=torch.int32, device=dev)
+        # union hand-off: the selection kernel only ORs the rows' sets into a
+        # bitmap (two buffers alternating over the layers) and the UP / DOWN
+        # GEMMs derive the ids from it, so no compaction sits between top-k and
+        # the MLP.  Opt-in (default off): measured 1 % slower per step at B=16
+        # and B=64 (DOWN's id expansion costs more than the compaction it
+        # removes).  Needs the tensor-core UP path (B > 4),
+        # no TP, split MLP launches, an even number of layers (every layer of a
+        # sparse-MLP engine selects; layer ell uses buffer ell % 2, so a
+        # replayed step starts on the buffer the previous step's last layer
+        # cleared), D <= 32768.
+        can = (self.sparse_mlp and tp is None and self.mlp_backend == "split" and cfg.layers % 2 == 0
+               and cfg.ffn_dim <= 32768)
+        if union_handoff is None:
+            union_handoff = False
+        if union_handoff and not (can and batch > 4):
+            raise ConfigurationError("union_handoff needs a sparse MLP, batch > 4, no TP, mlp_backend='split', an "
+                                     "even number of layers and ffn_dim <= 32768")
+        self.union_handoff = bool(union_handoff)
+        if self.union_handoff:
+            self.union_bm = torch.zeros(2, (cfg.ffn_dim + 31) // 32, dtype=torch.int32, device=dev)
         # expected union size per layer: sizes the selective-MLP grids (0 =
         # the maximum).  Set from the device counts of the warm-up step that
         # precedes every capture, so it follows the actual |S| (not k)
@@ -433,6 +454,16 @@ class DecodeEngine:
                     r.logits_into(self.h, self.r_hid, self.r_logits)
                     n += 2
                 lo, hi = (0, cfg.ffn_dim) if self.tp is None else self.tp.ffn_range
+                if self.union_handoff and self.trace is None and self.record is None:
+                    par = ell % 2
+                    bm, other = self.union_bm[par], self.union_bm[1 - par]
+                    _lib.check(L.ps_select_union_bitmap(_lib.ptr(self.r_logits), _lib.ptr(out_bias), B, cfg.ffn_dim,
+                                                        cfg.ffn_dim, self.k_mlp[ell], 0.0, _lib.ptr(bm),
+                                                        _lib.ptr(other), st), "ps_select_union_bitmap")
+                    mlp_into_bitmap(lw.mlp, self.h, bm, cnt, self.hidden, self.x, residual=self.x,
+                                    expected=self.union_est[ell])
+                    n += 3
+                    continue
                 _lib.check(L.ps_select_union(_lib.ptr(self.r_logits), _lib.ptr(out_bias), B, cfg.ffn_dim, cfg.ffn_dim,
                                              self.k_mlp[ell], 0.0, _lib.ptr(self.su_ws), self.su_bytes,
                                              lo, hi, ROW_PAD, _lib.ptr(self.union_idx),

@@ -435,6 +435,20 @@ def mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor,
                        flags=_lib.PS_GG_A_READY)  # idx/count were written before the UP launch
 
 
+def mlp_into_bitmap(pk: PackedMLP, x2d: torch.Tensor, bitmap: torch.Tensor, count, hidden: torch.Tensor,
+                    out: torch.Tensor, residual=None, expected=0) -> None:
+    """:func:`mlp_into` over the union given as a selection BITMAP (the
+    union hand-off: ps_select_union_bitmap wrote it, PS_GG_BITMAP makes UP
+    and DOWN derive the ids on the device).  ``count`` (int32 device scalar
+    or None) receives the union size from UP."""
+    B, d = x2d.shape
+    gather_gemm_into(pk.w1t, bitmap, count, x2d, x2d.stride(0), pk.b1, B, pk.D_pad, d, _lib.PS_ACT_RELU, hidden,
+                     hidden.stride(0), splits=expected, tag="gg_up", flags=_lib.PS_GG_BITMAP)
+    gather_gemm_t_into(pk.w2t, bitmap, None, hidden, hidden.stride(0), pk.b2, B, d, pk.D_pad, out, out.stride(0),
+                       residual=residual, res_ld=0 if residual is None else residual.stride(0), splits=expected,
+                       tag="gg_down", flags=_lib.PS_GG_A_READY | _lib.PS_GG_BITMAP)
+
+
 def sparse_mlp_into(pk: PackedMLP, x2d: torch.Tensor, idx, count, hidden: torch.Tensor, out: torch.Tensor,
                     residual=None, tag: str = "mlp_chain") -> None:
     """The whole selective MLP in ONE launch (ps_sparse_mlp): UP over the

@@ -23,6 +23,7 @@ from paper_2505_14884_b200.engine import DecodeEngine, SparsityPolicy  # noqa: E
 from paper_2505_14884_b200.model import SHAPES, DeviceModel  # noqa: E402
 
 TRACED = {"ps_gather_gemm": "gemm", "ps_gather_gemm_t": "gemm", "ps_select_union": "topk",
+          "ps_select_union_bitmap": "topk",
           "ps_router_mlp_fused": "router", "ps_sha_decode": "sha",
           "ps_sparse_mlp": "chain", "ps_router_mlp": "chain"}
 
