@@ -99,7 +99,10 @@ def load():
                 f"{LIB_PATH} is missing: build it with `python -m paper_2505_14884_b200._build` "
                 "(or __graft_entry__.build()); there is no CPU fallback")
         lib = ctypes.CDLL(LIB_PATH)
+        variant = "PS_LIB_PATH" in os.environ  # an older experiment build may lack newer entry points
         for name, (res, args) in SIGNATURES.items():
+            if variant and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -132,8 +132,10 @@ PS_DEV float4 ld_dsmem_v4(uint32_t addr) {
 
 // LSU_A: the A operand (weights, gathered or dense) is streamed by 4 loader
 // warps with 16-byte cp.async (LDGSTS) while the TMA engine moves only the B
-// operand.  GATHER: A rows (UP) / K rows (DOWN) are selected by idx.
-template <int MODE, bool GATHER, bool LSU_A>
+// operand.  GATHER: A rows (UP) / K rows (DOWN) are selected by idx.  BMAP
+// (union hand-off, PS_GG_BITMAP): the ids come from the selection bitmap; a
+// separate instantiation, so the id-list path compiles exactly as before.
+template <int MODE, bool GATHER, bool LSU_A, bool BMAP = false>
 __global__ void __launch_bounds__(kThreads, 2)
     gather_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const GGParams p) {
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // ---- union hand-off: word-prefix popcounts of the selection bitmap, so
   // union position `pos` maps to its id with a binary search + __fns (no
   // compacted id list, no compaction on the selection kernel's tail)
-  if (GATHER && p.bm) {
+  if (BMAP) {
     const int nw = p.bm_words;
     const int per = (nw + kThreads - 1) / kThreads;
     const int w0 = tid * per;
@@ -267,8 +269,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     return w * 32 + (int)__fns(s_bw[w], 0u, pos - s_bpre[w] + 1);
   };
   // ---- device-side work partition (identical in every role and CTA of a cluster)
-  const int count = (GATHER && p.bm) ? s_bpre[p.bm_words] : (p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K));
-  if (MODE == MODE_UP && GATHER && p.bm && p.count_out && blockIdx.x == 0 && tid == 0) *p.count_out = count;
+  const int count = BMAP ? s_bpre[p.bm_words] : (p.count ? *p.count : (MODE == MODE_UP ? p.M : p.K));
+  if (MODE == MODE_UP && BMAP && p.count_out && blockIdx.x == 0 && tid == 0) *p.count_out = count;
   const int klimit = (MODE == MODE_UP) ? p.K : count;
   const int kbt = (klimit + BK - 1) / BK;
   const int live_m = (MODE == MODE_UP) ? (count + BM - 1) / BM : (p.M + BM - 1) / BM;
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // range; UP: its first tile) into shared memory with every thread, one word
   // each, so the loaders read them with one shared load
   int ids_p0 = 0, ids_n = 0;
-  if (GATHER && p.bm) {
+  if (BMAP) {
     if (MODE == MODE_DOWN) {
       ids_p0 = kb0 * BK;
       ids_n = min(count, (kb0 + nkb) * BK) - ids_p0;
@@ -383,11 +385,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int m0 = (t % live_m) * BM;
         const uint16_t* src[8];  // UP: this thread's 8 rows of the tile
         if (MODE == MODE_UP) {
-          int bw = (GATHER && p.bm && j > 0 && m0 + (lt >> 3) < count) ? bm_seek(m0 + (lt >> 3)) : 0;
+          int bw = (BMAP && j > 0 && m0 + (lt >> 3) < count) ? bm_seek(m0 + (lt >> 3)) : 0;
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const int gr = m0 + (lt >> 3) + 16 * r;
-            const int id = gr < count ? (GATHER ? (p.bm ? (j == 0 && gr - ids_p0 < ids_n ? (int)s_ids[gr - ids_p0]
+            const int id = gr < count ? (GATHER ? (BMAP ? (j == 0 && gr - ids_p0 < ids_n ? (int)s_ids[gr - ids_p0]
                                                                                          : bm_id(gr, bw))
                                                             : __ldg(p.idx + gr))
                                                 : gr)
@@ -401,8 +403,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const int kg = kb * BK + (lt >> 4) + 8 * r;
-            if (GATHER && p.bm && kg < count && kg - ids_p0 >= ids_n && dw < 0) dw = bm_seek(kg);
-            o[r] = kg < count ? (GATHER ? (p.bm ? (kg - ids_p0 < ids_n ? (int)s_ids[kg - ids_p0] : bm_id(kg, dw))
+            if (BMAP && kg < count && kg - ids_p0 >= ids_n && dw < 0) dw = bm_seek(kg);
+            o[r] = kg < count ? (GATHER ? (BMAP ? (kg - ids_p0 < ids_n ? (int)s_ids[kg - ids_p0] : bm_id(kg, dw))
                                                 : __ldg(p.idx + kg))
                                        : kg)
                               : -1;
@@ -515,14 +517,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int nrows = min(NB, p.N - n0);
       float my_bias[4] = {0.f, 0.f, 0.f, 0.f};
       bool my_live[4];
-      int ew = (MODE == MODE_UP && GATHER && p.bm && p.bias && j > 0 && m0 + my_m < count) ? bm_seek(m0 + my_m) : 0;
+      int ew = (MODE == MODE_UP && BMAP && p.bias && j > 0 && m0 + my_m < count) ? bm_seek(m0 + my_m) : 0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int gm = m0 + my_m + u;
         my_live[u] = (MODE == MODE_UP) ? gm < count : gm < p.M;
         if (my_live[u] && p.bias)
           my_bias[u] = __ldg(p.bias + ((MODE == MODE_UP && p.idx)
-                                           ? (p.bm ? (j == 0 && gm - ids_p0 < ids_n ? (int)s_ids[gm - ids_p0]
+                                           ? (BMAP ? (j == 0 && gm - ids_p0 < ids_n ? (int)s_ids[gm - ids_p0]
                                                                                     : bm_id(gm, ew))
                                                    : __ldg(p.idx + gm))
                                            : gm));
@@ -822,13 +824,13 @@ int make_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uin
   return r == CUDA_SUCCESS ? PS_OK : PS_ERR_VALUE;
 }
 
-template <int MODE, bool GATHER, bool LSU_A>
+template <int MODE, bool GATHER, bool LSU_A, bool BMAP = false>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const GGParams& prm, int cluster, int work_ctas,
              cudaStream_t st) {
   const size_t smem = smem_bytes(prm.NB, prm.stages) +
                       (prm.bm ? 4 * (2 * (size_t)prm.bm_words + 1 + kThreads / 32) + ((size_t)prm.ids_cap * 2 + 15) / 16 * 16
                               : 0);
-  auto kern = gather_gemm_kernel<MODE, GATHER, LSU_A>;
+  auto kern = gather_gemm_kernel<MODE, GATHER, LSU_A, BMAP>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
@@ -863,6 +865,7 @@ int launch(GGParams& prm, int64_t w_rows_n, int64_t w_cols, int64_t kx, int tile
   // bitmap mode: ids expanded up front (one more K block of margin for DOWN)
   prm.ids_cap = MODE == MODE_DOWN ? ((kbt_est + cluster - 1) / cluster + 1) * BK : BM;
   const bool lsu = g_lsu_mode == 2 || (g_lsu_mode == 1 && gather);
+  if (prm.bm) return launch_t<MODE, true, true, true>(ta, tb, prm, cluster, work, st);  // gg_bitmap checked lsu
   if (gather)
     return lsu ? launch_t<MODE, true, true>(ta, tb, prm, cluster, work, st)
                : launch_t<MODE, true, false>(ta, tb, prm, cluster, work, st);
