@@ -227,7 +227,7 @@ class DecodeEngine:
         # union hand-off: the selection kernel only ORs the rows' sets into a
         # bitmap (two buffers alternating over the layers) and the UP / DOWN
         # GEMMs derive the ids from it, so no compaction sits between top-k and
-        # the MLP.  Opt-in (default off): measured 1 % slower per step at B=16
+        # the MLP.  Opt-in (default off): measured ~3 % slower per step at B=16
         # and B=64 (DOWN's id expansion costs more than the compaction it
         # removes).  Needs the tensor-core UP path (B > 4),
         # no TP, split MLP launches, an even number of layers (every layer of a
