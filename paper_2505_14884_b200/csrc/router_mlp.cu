@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
     if (has1) {
       mbar_wait(p1done, 0);
       tc_fence_after();
+      if (tr && et == 0) tr[13] = r_time();
       float* dst = p.part + (size_t)s1 * NB * p.r + t1 * RBM + m;
       const bool live = t1 * RBM + m < p.r;
       for (int c0 = 0; c0 < NB; c0 += 16) {

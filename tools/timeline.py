@@ -164,7 +164,7 @@ def main():
         slots = {"ps_select_union": [(0, "start"), (5, "selected"), (7, "union")],
                  "ps_sha_decode": [(0, "start"), (1, "dep wait"), (2, "partition"), (4, "1st tile"), (3, "end")],
                  "ps_router_mlp_fused": [(0, "start"), (1, "prefetched"), (7, "dep. wait"), (12, "p1 mma"),
-                                         (2, "p1 written"), (3, "barrier1"), (10, "reduce in"), (11, "reduce out"),
+                                         (13, "p1 done"), (2, "p1 written"), (3, "barrier1"), (10, "reduce in"), (11, "reduce out"),
                                          (4, "barrier2"), (8, "p2 mma0"), (9, "p2 mmaN"), (5, "acc2 ready"),
                                          (6, "done")]}.get(
             name, [(0, "start"), (1, "setup"), (2, "1st stage"), (3, "mma issued"), (8, "acc ready"),
