@@ -4,7 +4,7 @@
 //   logits = hid W_out (+ b_out)     f32  (B, D)
 //
 // Decode routers are weight streams with tiny outputs (r = 1024 hidden units,
-// B <= 256 rows), so the cost is latency: two dependent GEMMs, each with a
+// B <= 128 rows), so the cost is latency: two dependent GEMMs, each with a
 // launch prologue, and W_in's K = d contraction split across CTAs.  Here:
 //   * grid = one CTA per W_out row tile (128 logit columns, <= #SMs), one CTA
 //     per SM (> 114 KB of shared memory), every CTA co-resident;
@@ -388,7 +388,7 @@ unsigned long long* g_router_trace = nullptr;
 using namespace ps;
 
 extern "C" size_t ps_router_mlp_fused_workspace_bytes(int B, int d, int r, int D) {
-  if (B < 1 || B > 256 || d < 64 || r < 128 || D < 1) return 0;
+  if (B < 1 || B > 128 || d < 64 || r < 128 || D < 1) return 0;  // B > 128: phase-1 buffers exceed shared memory
   const int NB = (B + 15) / 16 * 16;
   const int tiles1 = (r + RBM - 1) / RBM, grid = (D + RBM - 1) / RBM;
   if (grid > ps_num_sms()) return 0;
@@ -397,7 +397,7 @@ extern "C" size_t ps_router_mlp_fused_workspace_bytes(int B, int d, int r, int D
   return 256 + (size_t)s * NB * r * 4;
 }
 
-// Returns PS_ERR_UNSUPPORTED for shapes outside the fused kernel (B > 256,
+// Returns PS_ERR_UNSUPPORTED for shapes outside the fused kernel (B > 128,
 // D > 128 * #SMs, W_in slices of more than 4 K-blocks, d or r not a multiple of
 // 64); the caller then runs the two GEMMs separately.
 extern "C" int ps_router_mlp_fused(const void* w_in_t, const float* b_in, const void* w_out_t, const float* b_out,
@@ -406,7 +406,7 @@ extern "C" int ps_router_mlp_fused(const void* w_in_t, const float* b_in, const 
                                    void* stream) {
   if (!w_in_t || !w_out_t || !x || !hid || !logits || !ws || B < 1 || d < 1 || r < 1 || D < 1) return PS_ERR_VALUE;
   if (x_ld < d || hid_ld < r || lg_ld < D || x_ld % 8 || hid_ld % 8) return PS_ERR_VALUE;
-  if (B > 256 || d % RBK || r % RBM || (D + RBM - 1) / RBM > ps_num_sms()) return PS_ERR_UNSUPPORTED;
+  if (B > 128 || d % RBK || r % RBM || (D + RBM - 1) / RBM > ps_num_sms()) return PS_ERR_UNSUPPORTED;
   const size_t need = ps_router_mlp_fused_workspace_bytes(B, d, r, D);
   if (!need) return PS_ERR_UNSUPPORTED;
   if (ws_bytes < need) return PS_ERR_WORKSPACE;

@@ -83,3 +83,19 @@ def test_router_fused_unsupported_shapes_fall_back():
     assert r.fused_into(x, hid, lg) is False
     wide = _router(9216, 36864, 1024)  # OPT-66B: W_in slices of > 4 K-blocks, > 148 tiles
     assert wide.fused_bytes(64) == 0
+
+
+@pytest.mark.parametrize("B", [129, 256])
+def test_router_fused_declines_large_batches(B):
+    """B > 128 does not fit the kernel's shared memory: no workspace size,
+    PS_ERR_UNSUPPORTED from the entry point, fused_into returns False (the
+    engine then runs the two GEMMs)."""
+    from paper_2505_14884_b200 import _lib
+
+    r = _router(4096, 16384, 1024)
+    assert r.fused_bytes(B) == 0
+    assert _lib.load().ps_router_mlp_fused_workspace_bytes(B, 4096, 1024, 16384) == 0
+    x = torch.zeros(B, 4096, device="cuda").bfloat16()
+    hid = torch.zeros(B, 1024, dtype=torch.bfloat16, device="cuda")
+    lg = torch.zeros(B, 16384, device="cuda")
+    assert r.fused_into(x, hid, lg) is False
