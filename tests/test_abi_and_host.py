@@ -65,6 +65,19 @@ def test_host_side_argument_errors(lib):
     assert lib.ps_topk_rows(nullp, 0, 10, ctypes.c_int64(10), 1, nullp, nullp, nullp) == 1
     assert lib.ps_bitmap_compact(nullp, 64, 3, 64, 128, nullp, nullp, nullp) == 1
     assert lib.ps_head_router_topk(nullp, ctypes.c_int64(8), nullp, nullp, 1, 7, 8, 2, nullp, nullp, nullp) == 1
+    # the union hand-off: no bitmap, k > cols, the bitmap aliasing the buffer it clears
+    f = ctypes.c_float(0.0)
+    p1, p2 = ctypes.c_void_p(64), ctypes.c_void_p(4096)
+    assert lib.ps_select_union_bitmap(p1, nullp, 2, 64, ctypes.c_int64(64), 8, f, nullp, nullp, nullp) == 1
+    assert lib.ps_select_union_bitmap(p1, nullp, 2, 64, ctypes.c_int64(64), 65, f, p2, nullp, nullp) == 1
+    assert lib.ps_select_union_bitmap(p1, nullp, 2, 64, ctypes.c_int64(64), 8, f, p2, p2, nullp) == 1
+    assert lib.ps_select_union_bitmap(p1, nullp, 2, 40000, ctypes.c_int64(40000), 8, f, p2, nullp, nullp) == 5
+    # fused router: batches beyond its shared memory have no workspace size
+    lib.ps_router_mlp_fused_workspace_bytes.restype = ctypes.c_size_t
+    assert lib.ps_router_mlp_fused_workspace_bytes(129, 4096, 1024, 16384) == 0
+    # allreduce: world out of range, rank outside the world
+    assert lib.ps_allreduce_add_bf16(p2, p2, p2, p2, 0, 9, 1, 8, p2, ctypes.c_int64(8), nullp) == 1
+    assert lib.ps_allreduce_add_bf16(p2, p2, p2, p2, 2, 2, 1, 8, p2, ctypes.c_int64(8), nullp) == 1
 
 
 def test_status_to_exception_mapping():
