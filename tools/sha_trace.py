@@ -58,3 +58,17 @@ for kh in (16, 32):
         d = (v - t0) / 1e3
         print(f"   {nm:10s} min {d.min():8.2f} p10 {np.percentile(d, 10):8.2f} med {np.median(d):8.2f} "
               f"p90 {np.percentile(d, 90):8.2f} max {d.max():8.2f}")
+    # which CTAs form the tail?  (rows are indexed by blockIdx; the first B
+    # stream-K CTAs also zero the unselected heads of sequence bid)
+    rows = bufs[1].view(-1, 8).cpu().numpy()
+    bid = np.arange(len(rows))
+    ok = (rows[:, 0] > 0) & (rows[:, 3] > 0)
+    end = (rows[:, 3] - t0) / 1e3
+    part = (rows[:, 2] - t0) / 1e3
+    zf = ok & (bid < B)
+    nz = ok & (bid >= B)
+    print(f"   zero-fill CTAs (bid < {B}): partition med {np.median(part[zf]):.2f} end med {np.median(end[zf]):.2f} "
+          f"max {end[zf].max():.2f} | others: partition med {np.median(part[nz]):.2f} end med "
+          f"{np.median(end[nz]):.2f} max {end[nz].max():.2f}")
+    late = np.argsort(end * ok)[-12:]
+    print("   latest CTAs (bid:end):", " ".join(f"{i}:{end[i]:.1f}" for i in late))
